@@ -1,0 +1,274 @@
+// extern "C" boundary of the B200 hot path (declared in include/riesz_mgrit_b200.h).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "riesz_mgrit_b200.h"
+#include "rm_kernels.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  return RM_ECUDA;
+}
+
+#define RM_CUDA(call, what)                     \
+  do {                                          \
+    cudaError_t e_ = (call);                    \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+const int kGroups[5] = {1, 2, 4, 8, 16};
+
+int padded_order(int nx, int ny) {
+  int n = std::max(nx, ny);
+  int np = 16;
+  while (np < n) np *= 2;
+  return np;
+}
+
+}  // namespace
+
+struct rm_grid {
+  int nx, ny, np, device;
+  double kx, ky, sx, sy, cm;
+  double* d_gens = nullptr;
+  double* d_scratch = nullptr;
+  int scratch_clusters = 0;
+  int* d_counter = nullptr;
+  int* d_fail = nullptr;
+  double* d_fail_info = nullptr;
+  int max_clusters[5] = {0, 0, 0, 0, 0};
+};
+
+extern "C" {
+
+const char* rm_version(void) { return "riesz_mgrit_b200 0.1.0 (sm_100a, FP64 DMMA)"; }
+
+const char* rm_last_error(void) { return g_err.c_str(); }
+
+int rm_max_order(void) { return 128; }
+
+int rm_grid_create(int nx, int ny, const double* t1x_col, const double* t1x_row, const double* t2x_col,
+                   const double* t2x_row, const double* t1y_col, const double* t1y_row, const double* t2y_col,
+                   const double* t2y_row, double sx, double sy, double kx, double ky, double mass_scale,
+                   rm_grid** out) {
+  if (!out) return fail(RM_EINVAL, "rm_grid_create: null output pointer");
+  *out = nullptr;
+  if (nx < 1 || ny < 1) return fail(RM_EINVAL, "rm_grid_create: need nx, ny >= 1");
+  if (!t1x_col || !t1x_row || !t2x_col || !t2x_row || !t1y_col || !t1y_row || !t2y_col || !t2y_row)
+    return fail(RM_EINVAL, "rm_grid_create: null generator");
+  const int np = padded_order(nx, ny);
+  if (np > rm_max_order())
+    return fail(RM_EUNSUP, "rm_grid_create: grid order " + std::to_string(std::max(nx, ny)) +
+                               " exceeds the supported maximum " + std::to_string(rm_max_order()));
+  rm_grid* g = new rm_grid();
+  g->nx = nx;
+  g->ny = ny;
+  g->np = np;
+  g->kx = kx;
+  g->ky = ky;
+  g->sx = sx;
+  g->sy = sy;
+  g->cm = mass_scale;
+  cudaGetDevice(&g->device);
+  // generator tables: entry (d + np) of table t, d in [-np, np+8)
+  const int GL = 2 * np + 8;
+  std::vector<double> tab(6 * GL, 0.0);
+  // entry (d) of a Toeplitz block given by first column/row: T[i][k] = t(i - k)
+  auto t2 = [](const double* col, const double* row, int d) { return d >= 0 ? col[d] : row[-d]; };
+  const double fx = kx * sx, fy = ky * sy;
+  for (int d = -np; d < np + 8; ++d) {
+    const int idx = d + np;
+    if (std::abs(d) < nx) {
+      tab[0 * GL + idx] = fx * t2(t1x_col, t1x_row, d);
+      tab[1 * GL + idx] = fx * t2(t2x_col, t2x_row, d);
+      tab[2 * GL + idx] = fx * t2(t2x_col, t2x_row, -d);
+    }
+    if (std::abs(d) < ny) {
+      tab[3 * GL + idx] = fy * t2(t1y_col, t1y_row, d);
+      tab[4 * GL + idx] = fy * t2(t2y_col, t2y_row, d);
+      tab[5 * GL + idx] = fy * t2(t2y_col, t2y_row, -d);
+    }
+  }
+  cudaError_t e;
+  int maxc = 1;
+  for (int gi = 0; gi < 5; ++gi) {
+    const int G = kGroups[gi];
+    if (!rm::chain_supported(np, G)) continue;
+    int n = 0;
+    e = rm::chain_max_clusters(np, G, &n);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    g->max_clusters[gi] = n;
+    maxc = std::max(maxc, n);
+  }
+  g->scratch_clusters = maxc;
+  if ((e = cudaMalloc(&g->d_gens, sizeof(double) * tab.size())) != cudaSuccess ||
+      (e = cudaMemcpy(g->d_gens, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMalloc(&g->d_scratch, sizeof(double) * 3 * (size_t)np * np * maxc)) != cudaSuccess ||
+      (e = cudaMalloc(&g->d_counter, sizeof(int))) != cudaSuccess ||
+      (e = cudaMalloc(&g->d_fail, sizeof(int))) != cudaSuccess ||
+      (e = cudaMemset(g->d_fail, 0, sizeof(int))) != cudaSuccess ||
+      (e = cudaMalloc(&g->d_fail_info, 4 * sizeof(double))) != cudaSuccess) {
+    rm_grid_destroy(g);
+    return cuda_fail(e, "rm_grid_create");
+  }
+  *out = g;
+  return RM_OK;
+}
+
+int rm_grid_destroy(rm_grid* g) {
+  if (!g) return RM_OK;
+  cudaFree(g->d_gens);
+  cudaFree(g->d_scratch);
+  cudaFree(g->d_counter);
+  cudaFree(g->d_fail);
+  cudaFree(g->d_fail_info);
+  delete g;
+  return RM_OK;
+}
+
+int rm_apply_batched(const rm_grid* g, int which, int batch, const double* d_dt, int sign, const double* d_v,
+                     int64_t v_stride, double* d_out, int64_t out_stride, void* stream) {
+  if (!g) return fail(RM_EINVAL, "rm_apply_batched: null grid");
+  if (which < 0 || which > 3) return fail(RM_EINVAL, "rm_apply_batched: which must be 0..3");
+  if (which == 0 && sign != 1 && sign != -1) return fail(RM_EINVAL, "sign must be +1 or -1");
+  if (batch < 0) return fail(RM_EINVAL, "rm_apply_batched: negative batch");
+  if (batch == 0) return RM_OK;
+  if (!d_v || !d_out || (which == 0 && !d_dt)) return fail(RM_EINVAL, "rm_apply_batched: null pointer");
+  rm::ApplyArgs a;
+  a.nx = g->nx;
+  a.ny = g->ny;
+  a.which = which;
+  a.sign = sign;
+  a.cm = g->cm;
+  a.kx = g->kx;
+  a.ky = g->ky;
+  a.gens = g->d_gens;
+  a.dt = d_dt;
+  a.v = d_v;
+  a.v_stride = v_stride;
+  a.out = d_out;
+  a.out_stride = out_stride;
+  RM_CUDA(rm::launch_apply(g->np, a, batch, (cudaStream_t)stream), "rm_apply_batched");
+  return RM_OK;
+}
+
+static int choose_group(const rm_grid* g, int nchains) {
+  // relative per-iteration time of one CTA holding the whole vector
+  const double t1 = 100.0 * pow(g->np / 128.0, 3.0);
+  double best = 1e300;
+  int best_g = 1;
+  for (int gi = 0; gi < 5; ++gi) {
+    const int G = kGroups[gi];
+    if (!rm::chain_supported(g->np, G) || g->max_clusters[gi] <= 0) continue;
+    const int slots = g->max_clusters[gi];
+    const double waves = ceil((double)nchains / slots);
+    const int units_per_cta = (g->np / 16) * (g->np / 16) / G;
+    const double eff = units_per_cta >= 8 ? 1.0 : 8.0 / units_per_cta * 0.6;
+    const double est = waves * (t1 / G * eff + (G > 1 ? 1.5 + 0.1 * G : 0.3));
+    if (est < best * 0.97) {
+      best = est;
+      best_g = G;
+    }
+  }
+  return best_g;
+}
+
+int rm_sweep_run(rm_grid* g, const rm_sweep* sw, void* stream) {
+  if (!g || !sw) return fail(RM_EINVAL, "rm_sweep_run: null argument");
+  if (sw->nchains <= 0) return RM_OK;
+  if (!sw->d_dt) return fail(RM_EINVAL, "rm_sweep_run: d_dt is required");
+  if (sw->clen < 1 || sw->first < 1 || sw->nmax < sw->first) return fail(RM_EINVAL, "rm_sweep_run: bad chain shape");
+  if (sw->out_div < 1) return fail(RM_EINVAL, "rm_sweep_run: out_div must be >= 1");
+  if ((sw->explicit_rhs || sw->x0_mode == 1) && !sw->d_src) return fail(RM_EINVAL, "rm_sweep_run: d_src required");
+  if (sw->x0_mode < 0 || sw->x0_mode > 2) return fail(RM_EINVAL, "rm_sweep_run: x0_mode must be 0, 1 or 2");
+  if (sw->x0_mode == 2 && !sw->d_x0) return fail(RM_EINVAL, "rm_sweep_run: d_x0 required for x0_mode 2");
+  if (sw->clen > 1 && (!sw->d_out || sw->out_div != 1))
+    return fail(RM_EINVAL, "rm_sweep_run: chains longer than one step need d_out with out_div == 1");
+  if (!sw->d_counters) return fail(RM_EINVAL, "rm_sweep_run: d_counters is required");
+  if (!(sw->rel_tol > 0)) return fail(RM_EINVAL, "relative tolerance must be positive");
+  int G = sw->group > 0 ? sw->group : choose_group(g, sw->nchains);
+  if (!rm::chain_supported(g->np, G))
+    return fail(RM_EUNSUP, "rm_sweep_run: group size " + std::to_string(G) + " unsupported for order " +
+                               std::to_string(g->np));
+  int gi = 0;
+  while (kGroups[gi] != G) ++gi;
+  int slots = g->max_clusters[gi];
+  if (slots <= 0) return fail(RM_EUNSUP, "rm_sweep_run: no resident cluster of size " + std::to_string(G));
+  slots = std::min(slots, g->scratch_clusters);
+  cudaStream_t st = (cudaStream_t)stream;
+  rm::ChainArgs a;
+  a.sw = *sw;
+  a.nx = g->nx;
+  a.ny = g->ny;
+  a.cm = g->cm;
+  a.gens = g->d_gens;
+  a.scratch = g->d_scratch;
+  a.chain_counter = g->d_counter;
+  a.fail = g->d_fail;
+  a.fail_info = g->d_fail_info;
+  RM_CUDA(cudaMemsetAsync(g->d_counter, 0, sizeof(int), st), "rm_sweep_run: counter reset");
+  RM_CUDA(rm::launch_chain(g->np, G, a, slots, st), "rm_sweep_run: launch");
+  return RM_OK;
+}
+
+int rm_fail_info(rm_grid* g, int* code, int* n, int64_t* iterations, double* residual_norm) {
+  if (!g) return fail(RM_EINVAL, "rm_fail_info: null grid");
+  int flag = 0;
+  double info[3] = {0, 0, 0};
+  RM_CUDA(cudaMemcpy(&flag, g->d_fail, sizeof(int), cudaMemcpyDeviceToHost), "rm_fail_info");
+  if (!flag) return 0;
+  RM_CUDA(cudaMemcpy(info, g->d_fail_info, 3 * sizeof(double), cudaMemcpyDeviceToHost), "rm_fail_info");
+  if (code) *code = flag;
+  if (n) *n = (int)info[0];
+  if (iterations) *iterations = (int64_t)info[1];
+  if (residual_norm) *residual_norm = info[2];
+  return 1;
+}
+
+int rm_fail_reset(rm_grid* g, void* stream) {
+  if (!g) return fail(RM_EINVAL, "rm_fail_reset: null grid");
+  RM_CUDA(cudaMemsetAsync(g->d_fail, 0, sizeof(int), (cudaStream_t)stream), "rm_fail_reset");
+  return RM_OK;
+}
+
+int rm_correct(int ndof, int nc, int m, double* d_u, int64_t u_stride, const double* d_uc, int64_t uc_stride,
+               void* stream) {
+  if (ndof < 1 || nc < 0 || m < 1 || !d_u || !d_uc) return fail(RM_EINVAL, "rm_correct: bad argument");
+  RM_CUDA(rm::launch_correct(ndof, nc, m, d_u, u_stride, d_uc, uc_stride, (cudaStream_t)stream), "rm_correct");
+  return RM_OK;
+}
+
+int rm_diff_sqnorm(int64_t n, const double* d_a, const double* d_b, double* d_out, void* stream) {
+  if (n < 0 || !d_a || !d_b || !d_out) return fail(RM_EINVAL, "rm_diff_sqnorm: bad argument");
+  RM_CUDA(rm::launch_diff_sqnorm(n, d_a, d_b, d_out, (cudaStream_t)stream), "rm_diff_sqnorm");
+  return RM_OK;
+}
+
+int rm_pcg64_uniform(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t start,
+                     int64_t count, int64_t row, double* d_out, int64_t out_stride, void* stream) {
+  if (count < 0 || start < 0 || row < 1 || !d_out) return fail(RM_EINVAL, "rm_pcg64_uniform: bad argument");
+  if (count == 0) return RM_OK;
+  rm::PcgArgs a{state_hi, state_lo, inc_hi, inc_lo, start, count, row, d_out, out_stride};
+  RM_CUDA(rm::launch_pcg64(a, (cudaStream_t)stream), "rm_pcg64_uniform");
+  return RM_OK;
+}
+
+}  // extern "C"

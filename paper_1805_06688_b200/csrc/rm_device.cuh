@@ -1,0 +1,203 @@
+// Device building blocks of the B200 hot path: tile configuration, the DMMA
+// block-Toeplitz matvec, the 7-point mass stencil and deterministic
+// cluster-wide reductions.
+//
+// Operator (assembly.py:100-115, 155-161).  On the 2-D view
+// V[j][i] (x fastest) the combined step operator is
+//   (A v)[j][i] = cm * mass(V)[j][i] + s * ( X[j][i] + Y[j][i] ),  s = sign*dt/2
+//   X[j][i] = sum_k  gx0(i-k) V[j][k] + gxp(i-k) V[j+1][k] + gxm(i-k) V[j-1][k]
+//   Y[j][i] = sum_l  gy0(j-l) V[l][i] + gyp(j-l) V[l][i+1] + gym(j-l) V[l][i-1]
+// with gx0(d) = kx*sx*t1x(d), gxp(d) = kx*sx*t2x(d), gxm(d) = gxp(-d), where
+// t(d) is a Toeplitz block entry T[i][k], d = i - k (first column for d >= 0,
+// first row for d < 0; T1 = A1 is symmetric), same along y.
+// Both contractions run as FP64 tensor-core MMAs (mma.sync m16n8k4 -> SASS
+// DMMA.8x8x4; sm_100a has no tcgen05 kind for f64).  The Toeplitz operand
+// fragments are read straight from O(n) generator tables in shared memory
+// (no n x n matrix is ever materialised); the vector operand is a zero-haloed
+// [NP+2][NP+4] tile in shared memory.
+//
+// Work decomposition.  The padded NP x NP output is cut into 16 x 16 "units".
+// A unit is always computed by one warp with the m16n8k4 fragment layout, the
+// K loop always runs x-segments (0,+1,-1) then y-segments (0,+1,-1) in
+// ascending k, and dot products are reduced per unit (lane order fixed) and
+// then over units in unit-index order.  A chain may be processed by a
+// cluster of G = 1..16 CTAs (each owns a band of units); the arithmetic of
+// every element and every dot product is independent of G, so results are
+// bitwise identical whatever group size (or GPU count) the host picks.
+#pragma once
+
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rm {
+
+namespace cgx = cooperative_groups;
+
+constexpr int UNIT = 16;
+
+template <int NP_, int G_>
+struct Cfg {
+  static constexpr int NP = NP_;
+  static constexpr int G = G_;
+  static constexpr int UR = NP / UNIT;  // units per row / column
+  static constexpr int U = UR * UR;     // units per vector
+  static constexpr int CR = (G <= UR) ? UR / G : 1;
+  static constexpr int CC = (G <= UR) ? UR : UR / (G / UR);
+  static constexpr int CU = CR * CC;  // units per CTA
+  static constexpr int WR = CU >= 32 ? 2 : 1;
+  static constexpr int WC = CU >= 64 ? 4 : (CU >= 16 ? 2 : 1);
+  static constexpr int WARPS = CU / (WR * WC);
+  static constexpr int THREADS = WARPS * 32;
+  static constexpr int NF = 2 * WC;  // 8-wide n-fragments per warp
+  static constexpr int S = NP + 4;   // Vt row stride in doubles (== 4 mod 16: conflict-free fragments)
+  static constexpr int VT = (NP + 2) * S;
+  static constexpr int GL = 2 * NP + 8;  // generator table length
+  static constexpr int RED = 2 * 4 * U;  // two reduction buffers of up to 4 values per unit
+  static constexpr size_t SMEM = sizeof(double) * (VT + 6 * GL + RED) + 64;
+  static_assert(G * CU == U, "CTA tiling");
+  static_assert(CR % WR == 0 && CC % WC == 0, "warp tiling");
+  static_assert(WARPS >= 1 && WARPS <= 8, "warps");
+};
+
+__device__ __forceinline__ void dmma(double (&c)[4], double a0, double a1, double b0) {
+  asm("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
+// Vt element (row j, col i), j,i may be -1..NP
+template <class C>
+__device__ __forceinline__ int vt_idx(int j, int i) {
+  return (j + 1) * C::S + i + 2;
+}
+
+// acc[mr][nf][e] = X + Y over the warp's units (see file comment).
+template <class C>
+__device__ __forceinline__ void matvec(const double* __restrict__ Vt, const double* __restrict__ gens,
+                                       double (&acc)[C::WR][C::NF][4], int urow, int ucol, int gq, int tig,
+                                       int kx_end, int ky_end, bool do_x, bool do_y) {
+#pragma unroll
+  for (int mr = 0; mr < C::WR; ++mr)
+#pragma unroll
+    for (int nf = 0; nf < C::NF; ++nf)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[mr][nf][e] = 0.0;
+  if (do_x) {
+#pragma unroll 1
+    for (int seg = 0; seg < 3; ++seg) {
+      const int delta = seg == 0 ? 0 : (seg == 1 ? 1 : -1);
+      const double* tab = gens + seg * C::GL + C::NP + 16 * ucol + gq - tig;
+      const double* ar[C::WR];
+#pragma unroll
+      for (int mr = 0; mr < C::WR; ++mr) ar[mr] = Vt + vt_idx<C>(16 * (urow + mr) + gq + delta, tig);
+#pragma unroll 4
+      for (int k0 = 0; k0 < kx_end; k0 += 4) {
+        double a[C::WR][2], b[C::NF];
+#pragma unroll
+        for (int mr = 0; mr < C::WR; ++mr) {
+          a[mr][0] = ar[mr][k0];
+          a[mr][1] = ar[mr][k0 + 8 * C::S];
+        }
+#pragma unroll
+        for (int nf = 0; nf < C::NF; ++nf) b[nf] = tab[8 * nf - k0];
+#pragma unroll
+        for (int mr = 0; mr < C::WR; ++mr)
+#pragma unroll
+          for (int nf = 0; nf < C::NF; ++nf) dmma(acc[mr][nf], a[mr][0], a[mr][1], b[nf]);
+      }
+    }
+  }
+  if (do_y) {
+#pragma unroll 1
+    for (int seg = 0; seg < 3; ++seg) {
+      const int delta = seg == 0 ? 0 : (seg == 1 ? 1 : -1);
+      const double* tab = gens + (3 + seg) * C::GL + C::NP + gq - tig;
+      const double* br = Vt + vt_idx<C>(tig, 16 * ucol + gq + delta);
+#pragma unroll 4
+      for (int l0 = 0; l0 < ky_end; l0 += 4) {
+        double a[C::WR][2], b[C::NF];
+#pragma unroll
+        for (int mr = 0; mr < C::WR; ++mr) {
+          a[mr][0] = tab[16 * (urow + mr) - l0];
+          a[mr][1] = tab[16 * (urow + mr) + 8 - l0];
+        }
+#pragma unroll
+        for (int nf = 0; nf < C::NF; ++nf) b[nf] = br[l0 * C::S + 8 * nf];
+#pragma unroll
+        for (int mr = 0; mr < C::WR; ++mr)
+#pragma unroll
+          for (int nf = 0; nf < C::NF; ++nf) dmma(acc[mr][nf], a[mr][0], a[mr][1], b[nf]);
+      }
+    }
+  }
+}
+
+// cm * (6 V(j,i) + V(j,i-1) + V(j,i+1) + V(j+1,i) + V(j+1,i+1) + V(j-1,i) + V(j-1,i-1))
+// (mass_generators, assembly.py:172-187, applied as a 7-point stencil).
+template <class C>
+__device__ __forceinline__ double mass_stencil(const double* __restrict__ Vt, int j, int i, double cm) {
+  const double* c = Vt + vt_idx<C>(j, i);
+  double s = 6.0 * c[0];
+  s += c[-1];
+  s += c[1];
+  s += c[C::S];
+  s += c[C::S + 1];
+  s += c[-C::S];
+  s += c[-C::S - 1];
+  return cm * s;
+}
+
+__device__ __forceinline__ double warp_allsum(double x) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+  return x;
+}
+
+template <int G>
+__device__ __forceinline__ void group_sync() {
+  if constexpr (G == 1) {
+    __syncthreads();
+  } else {
+    cgx::this_cluster().sync();
+  }
+}
+
+// Deterministic group-wide sum of NV values.  part[v][mr][uc] is this
+// thread's partial for unit (urow+mr, ucol+uc); the unit total is formed by a
+// fixed xor-butterfly, published to every CTA of the group, and the group
+// total is a fixed-order tree over unit indices (independent of G).
+template <class C, int NV>
+__device__ __forceinline__ void group_reduce(double (&part)[NV][C::WR][C::WC], double* red_local,
+                                             double* const* red_peer, int buf, int urow, int ucol, int lane,
+                                             double (&out)[NV]) {
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+#pragma unroll
+    for (int mr = 0; mr < C::WR; ++mr)
+#pragma unroll
+      for (int uc = 0; uc < C::WC; ++uc) part[v][mr][uc] = warp_allsum(part[v][mr][uc]);
+  if (lane == 0) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+#pragma unroll
+      for (int mr = 0; mr < C::WR; ++mr)
+#pragma unroll
+        for (int uc = 0; uc < C::WC; ++uc) {
+          const int u = (urow + mr) * C::UR + ucol + uc;
+#pragma unroll
+          for (int q = 0; q < C::G; ++q) red_peer[q][buf * 4 * C::U + v * C::U + u] = part[v][mr][uc];
+        }
+  }
+  group_sync<C::G>();
+  const double* r = red_local + buf * 4 * C::U;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    double x = 0.0;
+    if (lane < C::U) x = r[v * C::U + lane];
+    if (lane + 32 < C::U) x += r[v * C::U + lane + 32];
+    out[v] = warp_allsum(x);
+  }
+}
+
+}  // namespace rm

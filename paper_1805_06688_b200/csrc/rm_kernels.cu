@@ -1,0 +1,667 @@
+// B200 kernels of the MGRIT fine-propagator hot path (sm_100a).
+//
+//  chain_kernel : persistent kernel; each cluster of G CTAs pulls propagation
+//                 chains from a work counter and runs, per time step, the
+//                 explicit apply, the reference-exact CG solve and the MGRIT
+//                 epilogue (add G_n / subtract U_n / squared norm) without
+//                 leaving the SM: the iterate, residual and rhs live in a
+//                 fragment-native scratch (L2 resident), the search direction
+//                 lives in shared memory (broadcast to the cluster over DSMEM).
+//  apply_kernel : batched operator apply (CombinedStepOperator.apply / BttbOperator.apply).
+//  pcg64_kernel : numpy-bit-exact PCG64 uniform doubles (initial guess).
+//  correct_kernel, diff_sqnorm_kernel : small MGRIT helpers.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "riesz_mgrit_b200.h"
+#include "rm_device.cuh"
+#include "rm_kernels.h"
+
+namespace rm {
+
+// ----------------------------------------------------------------------------
+// chain kernel
+// ----------------------------------------------------------------------------
+
+template <class C>
+struct Ctx {
+  int tid, lane, warp, gq, tig, rank;
+  int urow, ucol;  // first unit (row, col) of this warp
+};
+
+#define RM_FOR_ELEM                                \
+  _Pragma("unroll") for (int mr = 0; mr < C::WR; ++mr) \
+  _Pragma("unroll") for (int nf = 0; nf < C::NF; ++nf) \
+  _Pragma("unroll") for (int e = 0; e < 4; ++e)
+
+template <class C>
+__device__ __forceinline__ int elem_row(const Ctx<C>& c, int mr, int e) {
+  return 16 * (c.urow + mr) + c.gq + 8 * (e >> 1);
+}
+template <class C>
+__device__ __forceinline__ int elem_col(const Ctx<C>& c, int nf, int e) {
+  return 16 * c.ucol + 8 * nf + 2 * c.tig + (e & 1);
+}
+template <class C>
+__device__ __forceinline__ int elem_sidx(const Ctx<C>& c, int mr, int nf, int e) {
+  return (((c.urow + mr) * C::UR + c.ucol + (nf >> 1)) * 256) + (((nf & 1) * 4 + e) * 32) + c.lane;
+}
+
+template <class C>
+__device__ __forceinline__ void load_vec(double* Vt, const double* __restrict__ src, int nx, int ny,
+                                         const Ctx<C>& c) {
+  for (int j = c.warp; j < ny; j += C::WARPS) {
+    const double* row = src + (int64_t)j * nx;
+    double* dst = Vt + vt_idx<C>(j, 0);
+    for (int i = c.lane; i < nx; i += 32) dst[i] = __ldcg(row + i);
+  }
+}
+
+template <class C>
+__device__ __forceinline__ void put_elem(double* const* vt_peer, int idx, double v) {
+#pragma unroll
+  for (int q = 0; q < C::G; ++q) vt_peer[q][idx] = v;
+}
+
+template <class C>
+__device__ __forceinline__ void zero_part(double (&p)[C::WR][C::WC]) {
+#pragma unroll
+  for (int mr = 0; mr < C::WR; ++mr)
+#pragma unroll
+    for (int uc = 0; uc < C::WC; ++uc) p[mr][uc] = 0.0;
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P) {
+  extern __shared__ __align__(16) double smem[];
+  double* Vt = smem;
+  double* gens = Vt + C::VT;
+  double* red = gens + 6 * C::GL;
+  int* sched = reinterpret_cast<int*>(red + C::RED);
+
+  Ctx<C> c;
+  c.tid = threadIdx.x;
+  c.lane = c.tid & 31;
+  c.warp = c.tid >> 5;
+  c.gq = c.lane >> 2;
+  c.tig = c.lane & 3;
+  c.rank = 0;
+  if constexpr (C::G > 1) c.rank = (int)cgx::this_cluster().block_rank();
+  {
+    int r0, c0;
+    if constexpr (C::G <= C::UR) {
+      r0 = c.rank * C::CR;
+      c0 = 0;
+    } else {
+      constexpr int per = C::G / C::UR;
+      r0 = c.rank / per;
+      c0 = (c.rank % per) * C::CC;
+    }
+    constexpr int wcols = C::CC / C::WC;
+    c.urow = r0 + (c.warp / wcols) * C::WR;
+    c.ucol = c0 + (c.warp % wcols) * C::WC;
+  }
+
+  double* vt_peer[C::G];
+  double* red_peer[C::G];
+  int* sched_peer[C::G];
+  if constexpr (C::G == 1) {
+    vt_peer[0] = Vt;
+    red_peer[0] = red;
+    sched_peer[0] = sched;
+  } else {
+    auto cl = cgx::this_cluster();
+#pragma unroll
+    for (int q = 0; q < C::G; ++q) {
+      vt_peer[q] = cl.map_shared_rank(Vt, q);
+      red_peer[q] = cl.map_shared_rank(red, q);
+      sched_peer[q] = cl.map_shared_rank(sched, q);
+    }
+  }
+
+  const rm_sweep& W = P.sw;
+  const int nx = P.nx, ny = P.ny;
+  const int ndof = nx * ny;
+  const int kx_end = (nx + 3) & ~3, ky_end = (ny + 3) & ~3;
+  const double cm = P.cm;
+  const int64_t max_iter = W.max_iter > 0 ? W.max_iter : 10 * (int64_t)ndof;
+
+  for (int i = c.tid; i < C::VT; i += C::THREADS) Vt[i] = 0.0;
+  for (int i = c.tid; i < 6 * C::GL; i += C::THREADS) gens[i] = P.gens[i];
+  group_sync<C::G>();
+
+  const int cid = blockIdx.x / C::G;
+  double* scr = P.scratch + (size_t)cid * 3 * C::NP * C::NP;
+  double* sx_ = scr;                         // iterate x
+  double* sr_ = scr + C::NP * C::NP;         // residual r
+  double* sb_ = scr + 2 * C::NP * C::NP;     // right-hand side b
+  int buf = 0;
+
+  double acc[C::WR][C::NF][4];
+
+  for (;;) {
+    if (c.rank == 0 && c.tid == 0) {
+      const int ch = atomicAdd(P.chain_counter, 1);
+#pragma unroll
+      for (int q = 0; q < C::G; ++q) sched_peer[q][0] = ch;
+    }
+    group_sync<C::G>();
+    const int chain = sched[0];
+    group_sync<C::G>();
+    if (chain >= W.nchains) break;
+
+    const int n0 = W.first + chain * W.cstride;
+    const int n1 = min(n0 + W.clen - 1, W.nmax);
+    bool chain_ok = true;
+    for (int n = n0; n <= n1 && chain_ok; ++n) {
+      const double s = 0.5 * W.d_dt[n - 1];
+      const double* in = (n == n0) ? W.d_src + (int64_t)(n - 1) * W.src_stride
+                                   : W.d_out + (int64_t)(n - 1) * W.out_stride;
+      const double fs = W.d_f ? (W.d_fscale ? W.d_fscale[n] : 1.0) : 0.0;
+      const double* Fn = W.d_f ? W.d_f + (int64_t)n * W.f_stride : nullptr;
+      const bool need_in = W.explicit_rhs || W.x0_mode == 1;
+
+      // ---------------- right-hand side, initial iterate and residual --------------
+      if (need_in) {
+        load_vec<C>(Vt, in, nx, ny, c);
+        __syncthreads();
+        matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true);
+      }
+      double part[2][C::WR][C::WC];
+      zero_part<C>(part[0]);
+      zero_part<C>(part[1]);
+      RM_FOR_ELEM {
+        const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
+        const bool ok = j < ny && i < nx;
+        const int si = elem_sidx<C>(c, mr, nf, e);
+        double b = 0.0, x = 0.0, r = 0.0;
+        if (ok) {
+          double mv = 0.0, kv = 0.0;
+          if (need_in) {
+            mv = mass_stencil<C>(Vt, j, i, cm);
+            kv = acc[mr][nf][e];
+          }
+          if (W.explicit_rhs) b = mv + (-s) * kv;
+          if (Fn) {
+            const double f = fs * __ldcg(Fn + j * nx + i);
+            b = W.explicit_rhs ? f + b : f;
+          }
+          if (W.x0_mode == 1) {
+            x = Vt[vt_idx<C>(j, i)];
+            r = b - (mv + s * kv);
+          } else {
+            r = b;  // x0 = 0: r = b - A*0 (krylov.py:47,50)
+          }
+        }
+        sb_[si] = b;
+        sx_[si] = x;
+        sr_[si] = r;
+        part[0][mr][nf >> 1] += b * b;
+        part[1][mr][nf >> 1] += r * r;
+      }
+      if (W.x0_mode == 2) {
+        // given initial iterate (spacetime_residual, stepper.py:203)
+        __syncthreads();
+        group_sync<C::G>();  // every CTA done with Vt before it is overwritten
+        load_vec<C>(Vt, W.d_x0 + (int64_t)n * W.x0_stride, nx, ny, c);
+        __syncthreads();
+        matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true);
+        zero_part<C>(part[1]);
+        RM_FOR_ELEM {
+          const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
+          const bool ok = j < ny && i < nx;
+          const int si = elem_sidx<C>(c, mr, nf, e);
+          double x = 0.0, r = 0.0;
+          if (ok) {
+            x = Vt[vt_idx<C>(j, i)];
+            r = sb_[si] - (mass_stencil<C>(Vt, j, i, cm) + s * acc[mr][nf][e]);
+          }
+          sx_[si] = x;
+          sr_[si] = r;
+          part[1][mr][nf >> 1] += r * r;
+        }
+      }
+      double tot[2];
+      group_reduce<C, 2>(part, red, red_peer, buf, c.urow, c.ucol, c.lane, tot);
+      buf ^= 1;
+      const double bnorm = sqrt(tot[0]);
+      const double target = bnorm > 0.0 ? W.rel_tol * bnorm : W.rel_tol;
+      double res = sqrt(tot[1]);
+      double rr = tot[1];
+      int64_t its = 0;
+      int fail = 0;
+      bool done = res <= target;
+
+      if (!done) {
+        // p = r into the shared operand tile of every CTA of the group
+        RM_FOR_ELEM {
+          const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
+          if (j < ny && i < nx) put_elem<C>(vt_peer, vt_idx<C>(j, i), sr_[elem_sidx<C>(c, mr, nf, e)]);
+        }
+        group_sync<C::G>();
+      }
+      for (int64_t k = 1; !done && !fail; ++k) {
+        if (k > max_iter) {
+          fail = RM_CG_BUDGET;
+          its = max_iter;
+          break;
+        }
+        // Ap and p'Ap
+        matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true);
+        double p1[1][C::WR][C::WC];
+        zero_part<C>(p1[0]);
+        RM_FOR_ELEM {
+          const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
+          double ap = 0.0;
+          if (j < ny && i < nx) {
+            ap = mass_stencil<C>(Vt, j, i, cm) + s * acc[mr][nf][e];
+            p1[0][mr][nf >> 1] += Vt[vt_idx<C>(j, i)] * ap;
+          }
+          acc[mr][nf][e] = ap;
+        }
+        double pap[1];
+        group_reduce<C, 1>(p1, red, red_peer, buf, c.urow, c.ucol, c.lane, pap);
+        buf ^= 1;
+        if (!isfinite(pap[0]) || pap[0] <= 0.0) {
+          fail = RM_CG_BREAKDOWN;
+          its = k;
+          break;
+        }
+        const double alpha = rr / pap[0];
+        zero_part<C>(p1[0]);
+        RM_FOR_ELEM {
+          const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
+          const int si = elem_sidx<C>(c, mr, nf, e);
+          if (j < ny && i < nx) {
+            const double pv = Vt[vt_idx<C>(j, i)];
+            const double xn = sx_[si] + alpha * pv;
+            const double rn = sr_[si] - alpha * acc[mr][nf][e];
+            sx_[si] = xn;
+            sr_[si] = rn;
+            p1[0][mr][nf >> 1] += rn * rn;
+          }
+        }
+        double rrn[1];
+        group_reduce<C, 1>(p1, red, red_peer, buf, c.urow, c.ucol, c.lane, rrn);
+        buf ^= 1;
+        double rr_new = rrn[0];
+        res = sqrt(rr_new);
+        if (!isfinite(res)) {
+          fail = RM_CG_NONFINITE;
+          its = k;
+          break;
+        }
+        if (res <= target) {
+          // acceptance on the true residual (krylov.py:71-83)
+          RM_FOR_ELEM {
+            const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
+            if (j < ny && i < nx) put_elem<C>(vt_peer, vt_idx<C>(j, i), sx_[elem_sidx<C>(c, mr, nf, e)]);
+          }
+          group_sync<C::G>();
+          matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true);
+          zero_part<C>(p1[0]);
+          RM_FOR_ELEM {
+            const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
+            const int si = elem_sidx<C>(c, mr, nf, e);
+            double rt = 0.0;
+            if (j < ny && i < nx) rt = sb_[si] - (mass_stencil<C>(Vt, j, i, cm) + s * acc[mr][nf][e]);
+            acc[mr][nf][e] = rt;
+            p1[0][mr][nf >> 1] += rt * rt;
+          }
+          double tt[1];
+          group_reduce<C, 1>(p1, red, red_peer, buf, c.urow, c.ucol, c.lane, tt);
+          buf ^= 1;
+          const double true_res = sqrt(tt[0]);
+          if (true_res <= fmax(target, 10.0 * res)) {
+            its = k;
+            done = true;
+            break;
+          }
+          // recurrence drifted: restart from the true residual
+          rr_new = tt[0];
+          res = true_res;
+          RM_FOR_ELEM {
+            const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
+            if (j < ny && i < nx) {
+              sr_[elem_sidx<C>(c, mr, nf, e)] = acc[mr][nf][e];
+              put_elem<C>(vt_peer, vt_idx<C>(j, i), acc[mr][nf][e]);
+            }
+          }
+          if (res <= target) {
+            its = k;
+            done = true;
+            break;
+          }
+          rr = rr_new;
+          group_sync<C::G>();
+          continue;
+        }
+        const double beta = rr_new / rr;
+        rr = rr_new;
+        RM_FOR_ELEM {
+          const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
+          if (j < ny && i < nx) {
+            const int vi = vt_idx<C>(j, i);
+            put_elem<C>(vt_peer, vi, sr_[elem_sidx<C>(c, mr, nf, e)] + beta * Vt[vi]);
+          }
+        }
+        group_sync<C::G>();
+      }
+
+      if (c.rank == 0 && c.tid == 0) {
+        atomicAdd(W.d_counters, 1ull);
+        atomicAdd(W.d_counters + 1, (unsigned long long)its);
+      }
+      if (fail) {
+        if (c.rank == 0 && c.tid == 0 && atomicCAS(P.fail, 0, fail) == 0) {
+          P.fail_info[0] = (double)n;
+          P.fail_info[1] = (double)its;
+          P.fail_info[2] = res;
+        }
+        chain_ok = false;
+        break;
+      }
+
+      // ---------------- MGRIT epilogue: y = [G_n +] x [- S_n] ----------------
+      const int oi = n / W.out_div;
+      const double* Gn = W.d_gadd ? W.d_gadd + (int64_t)n * W.gadd_stride : nullptr;
+      const double* Sn = W.d_sub ? W.d_sub + (int64_t)n * W.sub_stride : nullptr;
+      double* On = W.d_out ? W.d_out + (int64_t)oi * W.out_stride : nullptr;
+      double p1[1][C::WR][C::WC];
+      zero_part<C>(p1[0]);
+      RM_FOR_ELEM {
+        const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
+        if (j < ny && i < nx) {
+          const int gi = j * nx + i;
+          double y = sx_[elem_sidx<C>(c, mr, nf, e)];
+          if (Gn) y = __ldcg(Gn + gi) + y;
+          if (Sn) y = y - __ldcg(Sn + gi);
+          if (On) On[gi] = y;
+          p1[0][mr][nf >> 1] += y * y;
+        }
+      }
+      if (W.d_norms) {
+        double yy[1];
+        group_reduce<C, 1>(p1, red, red_peer, buf, c.urow, c.ucol, c.lane, yy);
+        buf ^= 1;
+        if (c.rank == 0 && c.tid == 0) W.d_norms[oi] = yy[0];
+      }
+      // make y visible to every CTA of the group before the next step loads it
+      __threadfence();
+      group_sync<C::G>();
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// batched apply
+// ----------------------------------------------------------------------------
+
+template <class C>
+__global__ void __launch_bounds__(C::THREADS, 1) apply_kernel(const ApplyArgs P) {
+  extern __shared__ __align__(16) double smem[];
+  double* Vt = smem;
+  double* gens = Vt + C::VT;
+  Ctx<C> c;
+  c.tid = threadIdx.x;
+  c.lane = c.tid & 31;
+  c.warp = c.tid >> 5;
+  c.gq = c.lane >> 2;
+  c.tig = c.lane & 3;
+  c.rank = 0;
+  constexpr int wcols = C::CC / C::WC;
+  c.urow = (c.warp / wcols) * C::WR;
+  c.ucol = (c.warp % wcols) * C::WC;
+  const int nx = P.nx, ny = P.ny;
+  for (int i = c.tid; i < C::VT; i += C::THREADS) Vt[i] = 0.0;
+  for (int i = c.tid; i < 6 * C::GL; i += C::THREADS) gens[i] = P.gens[i];
+  __syncthreads();
+  const int b = blockIdx.x;
+  load_vec<C>(Vt, P.v + (int64_t)b * P.v_stride, nx, ny, c);
+  __syncthreads();
+  double acc[C::WR][C::NF][4];
+  const bool dox = P.which == 0 || P.which == 2;
+  const bool doy = P.which == 0 || P.which == 3;
+  if (dox || doy)
+    matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, (nx + 3) & ~3, (ny + 3) & ~3, dox, doy);
+  double sc = 0.0;
+  if (P.which == 0) sc = P.sign * 0.5 * P.dt[b];
+  if (P.which == 2) sc = 1.0 / P.kx;
+  if (P.which == 3) sc = 1.0 / P.ky;
+  double* out = P.out + (int64_t)b * P.out_stride;
+  RM_FOR_ELEM {
+    const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
+    if (j < ny && i < nx) {
+      double y;
+      if (P.which == 1)
+        y = mass_stencil<C>(Vt, j, i, P.cm);
+      else if (P.which == 0)
+        y = mass_stencil<C>(Vt, j, i, P.cm) + sc * acc[mr][nf][e];
+      else
+        y = sc * acc[mr][nf][e];
+      out[j * nx + i] = y;
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// PCG64 (numpy default_rng bit generator: 128-bit LCG + XSL-RR output)
+// ----------------------------------------------------------------------------
+
+typedef unsigned __int128 u128;
+
+__device__ __forceinline__ void lcg_jump(u128 mult, u128 plus, uint64_t delta, u128& am, u128& ap) {
+  u128 acc_m = 1, acc_p = 0;
+  while (delta) {
+    if (delta & 1) {
+      acc_m *= mult;
+      acc_p = acc_p * mult + plus;
+    }
+    plus = (mult + 1) * plus;
+    mult *= mult;
+    delta >>= 1;
+  }
+  am = acc_m;
+  ap = acc_p;
+}
+
+__global__ void pcg64_kernel(PcgArgs P) {
+  const u128 MULT = ((u128)0x2360ED051FC65DA4ull << 64) | (u128)0x4385DF649FCCF645ull;
+  const u128 inc = ((u128)P.inc_hi << 64) | P.inc_lo;
+  const u128 s0 = ((u128)P.state_hi << 64) | P.state_lo;
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= P.count) return;
+  u128 am, ap;
+  // state after (start + t + 1) steps is the one whose output is draw (start + t)
+  lcg_jump(MULT, inc, (uint64_t)(P.start + t + 1), am, ap);
+  u128 s = am * s0 + ap;
+  u128 jm, jp;
+  lcg_jump(MULT, inc, (uint64_t)T, jm, jp);
+  for (int64_t i = t; i < P.count; i += T) {
+    const uint64_t hi = (uint64_t)(s >> 64), lo = (uint64_t)s;
+    const uint64_t x = hi ^ lo;
+    const unsigned rot = (unsigned)(s >> 122);
+    const uint64_t o = (x >> rot) | (x << ((64u - rot) & 63u));
+    const double d = (double)(o >> 11) * (1.0 / 9007199254740992.0);
+    P.out[(i / P.row) * P.out_stride + (i % P.row)] = d;
+    s = jm * s + jp;
+  }
+}
+
+// ----------------------------------------------------------------------------
+// helpers
+// ----------------------------------------------------------------------------
+
+__global__ void correct_kernel(int ndof, int nc, int m, double* u, int64_t us, const double* uc, int64_t ucs) {
+  const int64_t total = (int64_t)(nc + 1) * ndof;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = t / ndof, i = t % ndof;
+    u[k * m * us + i] += uc[k * ucs + i];
+  }
+}
+
+__global__ void diff_sqnorm_kernel(int64_t n, const double* a, const double* b, double* out) {
+  __shared__ double sm[32];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double d = a[i] - b[i];
+    s += d * d;
+  }
+  s = warp_allsum(s);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double x = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
+    x = warp_allsum(x);
+    if (threadIdx.x == 0) out[0] = x;
+  }
+}
+
+// ----------------------------------------------------------------------------
+// launch helpers (instantiations)
+// ----------------------------------------------------------------------------
+
+template <int NP, int G>
+static cudaError_t launch_chain_t(const ChainArgs& a, int max_clusters, cudaStream_t st) {
+  using C = Cfg<NP, G>;
+  auto kern = chain_kernel<C>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  if (err != cudaSuccess) return err;
+  if (G > 8) {
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (err != cudaSuccess) return err;
+  }
+  int ncl = max_clusters;
+  if (ncl > a.sw.nchains) ncl = a.sw.nchains;
+  if (ncl < 1) ncl = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ncl * G);
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = G;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+template <int NP, int G>
+static cudaError_t max_clusters_t(int* out) {
+  using C = Cfg<NP, G>;
+  auto kern = chain_kernel<C>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  if (err != cudaSuccess) return err;
+  if (G > 8) {
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (err != cudaSuccess) return err;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = G;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaOccupancyMaxActiveClusters(out, kern, &cfg);
+}
+
+#define RM_CHAIN_CASES(X) \
+  X(16, 1)                \
+  X(32, 1)                \
+  X(32, 2)                \
+  X(64, 1)                \
+  X(64, 2)                \
+  X(64, 4)                \
+  X(128, 1)               \
+  X(128, 2)               \
+  X(128, 4)               \
+  X(128, 8)               \
+  X(128, 16)
+
+bool chain_supported(int np, int g) {
+#define X(a, b) \
+  if (np == a && g == b) return true;
+  RM_CHAIN_CASES(X)
+#undef X
+  return false;
+}
+
+cudaError_t launch_chain(int np, int g, const ChainArgs& a, int max_clusters, cudaStream_t st) {
+#define X(A, B) \
+  if (np == A && g == B) return launch_chain_t<A, B>(a, max_clusters, st);
+  RM_CHAIN_CASES(X)
+#undef X
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t chain_max_clusters(int np, int g, int* out) {
+#define X(A, B) \
+  if (np == A && g == B) return max_clusters_t<A, B>(out);
+  RM_CHAIN_CASES(X)
+#undef X
+  return cudaErrorInvalidValue;
+}
+
+size_t chain_smem(int np, int g) {
+#define X(A, B) \
+  if (np == A && g == B) return Cfg<A, B>::SMEM;
+  RM_CHAIN_CASES(X)
+#undef X
+  return 0;
+}
+
+template <int NP>
+static cudaError_t launch_apply_t(const ApplyArgs& a, int batch, cudaStream_t st) {
+  using C = Cfg<NP, 1>;
+  auto kern = apply_kernel<C>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  if (err != cudaSuccess) return err;
+  kern<<<batch, C::THREADS, C::SMEM, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_apply(int np, const ApplyArgs& a, int batch, cudaStream_t st) {
+  switch (np) {
+    case 16: return launch_apply_t<16>(a, batch, st);
+    case 32: return launch_apply_t<32>(a, batch, st);
+    case 64: return launch_apply_t<64>(a, batch, st);
+    case 128: return launch_apply_t<128>(a, batch, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_pcg64(const PcgArgs& a, cudaStream_t st) {
+  int64_t threads = 256;
+  int64_t blocks = (a.count + threads - 1) / threads;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  pcg64_kernel<<<(unsigned)blocks, (unsigned)threads, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_correct(int ndof, int nc, int m, double* u, int64_t us, const double* uc, int64_t ucs,
+                           cudaStream_t st) {
+  const int64_t total = (int64_t)(nc + 1) * ndof;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) blocks = 1;
+  correct_kernel<<<(unsigned)blocks, 256, 0, st>>>(ndof, nc, m, u, us, uc, ucs);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_diff_sqnorm(int64_t n, const double* a, const double* b, double* out, cudaStream_t st) {
+  diff_sqnorm_kernel<<<1, 1024, 0, st>>>(n, a, b, out);
+  return cudaGetLastError();
+}
+
+}  // namespace rm

@@ -1,0 +1,51 @@
+// Internal kernel-launch interface (not part of the C ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "riesz_mgrit_b200.h"
+
+namespace rm {
+
+struct ChainArgs {
+  rm_sweep sw;
+  int nx, ny;
+  double cm;
+  const double* gens;  // 6 generator tables of length 2*NP+8 (device)
+  double* scratch;     // 3*NP*NP doubles per cluster (device)
+  int* chain_counter;  // work counter, zeroed before launch
+  int* fail;           // first-failure flag
+  double* fail_info;   // n, iterations, residual norm
+};
+
+struct ApplyArgs {
+  int nx, ny, which, sign;
+  double cm, kx, ky;
+  const double* gens;
+  const double* dt;
+  const double* v;
+  int64_t v_stride;
+  double* out;
+  int64_t out_stride;
+};
+
+struct PcgArgs {
+  uint64_t state_hi, state_lo, inc_hi, inc_lo;
+  int64_t start, count, row;
+  double* out;
+  int64_t out_stride;
+};
+
+bool chain_supported(int np, int g);
+cudaError_t launch_chain(int np, int g, const ChainArgs& a, int max_clusters, cudaStream_t st);
+cudaError_t chain_max_clusters(int np, int g, int* out);
+size_t chain_smem(int np, int g);
+cudaError_t launch_apply(int np, const ApplyArgs& a, int batch, cudaStream_t st);
+cudaError_t launch_pcg64(const PcgArgs& a, cudaStream_t st);
+cudaError_t launch_correct(int ndof, int nc, int m, double* u, int64_t us, const double* uc, int64_t ucs,
+                           cudaStream_t st);
+cudaError_t launch_diff_sqnorm(int64_t n, const double* a, const double* b, double* out, cudaStream_t st);
+
+}  // namespace rm
