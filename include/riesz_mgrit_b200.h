@@ -104,7 +104,8 @@ RM_API int rm_apply_batched(const rm_grid* grid, int which, int batch, const dou
  * rhs_vector (stepper.py:142-146), sequential_solve (:173-184) and
  * spacetime_residual (:187-205), each as one launch.
  * d_counters[0] += number of spatial solves, d_counters[1] += CG iterations
- * (Discretization.spatial_solves / cg_iterations, stepper.py:95-96,114,121).
+ * (Discretization.spatial_solves / cg_iterations, stepper.py:95-96,114,121),
+ * d_counters[2] += operator applies performed (for FLOP accounting).
  * A CG failure is recorded in the grid's failure slot (rm_fail_info).
  */
 typedef struct rm_sweep {

@@ -230,6 +230,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
       double res = sqrt(tot[1]);
       double rr = tot[1];
       int64_t its = 0;
+      int64_t nmv = (need_in ? 1 : 0) + (W.x0_mode == 2 ? 1 : 0);
       int fail = 0;
       bool done = res <= target;
 
@@ -249,6 +250,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
         }
         // Ap and p'Ap
         matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true);
+        ++nmv;
         double p1[1][C::WR][C::WC];
         zero_part<C>(p1[0]);
         RM_FOR_ELEM {
@@ -300,6 +302,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           }
           group_sync<C::G>();
           matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true);
+          ++nmv;
           zero_part<C>(p1[0]);
           RM_FOR_ELEM {
             const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
@@ -352,6 +355,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
       if (c.rank == 0 && c.tid == 0) {
         atomicAdd(W.d_counters, 1ull);
         atomicAdd(W.d_counters + 1, (unsigned long long)its);
+        atomicAdd(W.d_counters + 2, (unsigned long long)nmv);
       }
       if (fail) {
         if (c.rank == 0 && c.tid == 0 && atomicCAS(P.fail, 0, fail) == 0) {

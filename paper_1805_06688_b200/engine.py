@@ -99,6 +99,14 @@ class Engine:
                                               gens.mass_scale, C.byref(handle)), "rm_grid_create")
         self.handle = handle
         self.launches = 0
+        self.trace = None  # list of (tag, start event, end event, counters-before) when profiling
+
+    def start_trace(self):
+        self.trace = []
+
+    def stop_trace(self):
+        tr, self.trace = self.trace, None
+        return tr
 
     @classmethod
     def for_problem(cls, grid, beta, gamma, kx, ky) -> "Engine":
@@ -132,7 +140,7 @@ class Engine:
               x0_mode: int = 1, x0: torch.Tensor | None = None, f: torch.Tensor | None = None, f_stride: int = 0,
               fscale: torch.Tensor | None = None, gadd: torch.Tensor | None = None, sub: torch.Tensor | None = None,
               out: torch.Tensor | None = None, out_div: int = 1, norms: torch.Tensor | None = None,
-              max_iter: int | None = None, group: int = 0, row: int | None = None) -> None:
+              max_iter: int | None = None, group: int = 0, row: int | None = None, tag: str = "") -> None:
         """One rm_sweep_run launch; 2-D arrays are indexed by time point with row stride ``row``."""
         if nchains <= 0:
             return
@@ -153,12 +161,19 @@ class Engine:
         sw.d_norms = _ptr(norms, 1)
         sw.rel_tol = float(rel_tol)
         sw.max_iter = -1 if max_iter is None else int(max_iter)
-        if counters.dtype != torch.int64 or not counters.is_cuda:
-            raise TypeError("counters must be an int64 CUDA tensor")
+        if counters.dtype != torch.int64 or not counters.is_cuda or counters.numel() < 3:
+            raise TypeError("counters must be an int64 CUDA tensor of length 3")
         sw.d_counters = counters.data_ptr()
         sw.group = int(group)
+        if self.trace is not None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            before = counters.clone()
+            e0.record()
         _native.check(self.lib.rm_sweep_run(self.handle, C.byref(sw), _stream()), "rm_sweep_run")
         self.launches += 1
+        if self.trace is not None:
+            e1.record()
+            self.trace.append((tag, e0, e1, before, counters.clone(), nchains))
 
     def check_fail(self) -> None:
         """Raise CgFailure for the first failed solve since the last reset (synchronises)."""

