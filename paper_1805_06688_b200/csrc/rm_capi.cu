@@ -121,7 +121,7 @@ int rm_grid_create(int nx, int ny, const double* t1x_col, const double* t1x_row,
   g->scratch_clusters = maxc;
   if ((e = cudaMalloc(&g->d_gens, sizeof(double) * tab.size())) != cudaSuccess ||
       (e = cudaMemcpy(g->d_gens, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice)) != cudaSuccess ||
-      (e = cudaMalloc(&g->d_scratch, sizeof(double) * 3 * (size_t)np * np * maxc)) != cudaSuccess ||
+      (e = cudaMalloc(&g->d_scratch, sizeof(double) * (size_t)np * np * maxc)) != cudaSuccess ||
       (e = cudaMalloc(&g->d_counter, sizeof(int))) != cudaSuccess ||
       (e = cudaMalloc(&g->d_fail, sizeof(int))) != cudaSuccess ||
       (e = cudaMemset(g->d_fail, 0, sizeof(int))) != cudaSuccess ||

@@ -54,7 +54,9 @@ struct Cfg {
   static constexpr int VT = (NP + 2) * S;
   static constexpr int GL = 2 * NP + 8;  // generator table length
   static constexpr int RED = 2 * 4 * U;  // two reduction buffers of up to 4 values per unit
-  static constexpr size_t SMEM = sizeof(double) * (VT + 6 * GL + RED) + 64;
+  static constexpr int XS = CU * 256;    // CG iterate of this CTA's units (shared-memory resident)
+  static constexpr size_t SMEM = sizeof(double) * (VT + 6 * GL + RED + XS) + 64;
+  static constexpr size_t APPLY_SMEM = sizeof(double) * (VT + 6 * GL);
   static_assert(G * CU == U, "CTA tiling");
   static_assert(CR % WR == 0 && CC % WC == 0, "warp tiling");
   static_assert(WARPS >= 1 && WARPS <= 8, "warps");

@@ -73,12 +73,20 @@ __device__ __forceinline__ void zero_part(double (&p)[C::WR][C::WC]) {
 }
 
 template <class C>
+__device__ __forceinline__ int elem_xidx(const Ctx<C>& c, int mr, int nf, int e) {
+  // x lives in shared memory in fragment-native order (lane-contiguous: conflict free)
+  return (((c.warp * C::WR + mr) * C::WC + (nf >> 1)) * 8 + (nf & 1) * 4 + e) * 32 + c.lane;
+}
+
+template <class C>
 __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P) {
+  static_assert(C::SMEM <= 227 * 1024, "shared memory budget");
   extern __shared__ __align__(16) double smem[];
-  double* Vt = smem;
-  double* gens = Vt + C::VT;
-  double* red = gens + 6 * C::GL;
-  int* sched = reinterpret_cast<int*>(red + C::RED);
+  double* Vt = smem;                   // operand tile (p, or the vector being applied)
+  double* gens = Vt + C::VT;           // generator tables
+  double* red = gens + 6 * C::GL;      // reduction buffers
+  double* xs = red + C::RED;           // this CTA's part of the CG iterate x
+  int* sched = reinterpret_cast<int*>(xs + C::XS);
 
   Ctx<C> c;
   c.tid = threadIdx.x;
@@ -126,19 +134,18 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
   const int kx_end = (nx + 3) & ~3, ky_end = (ny + 3) & ~3;
   const double cm = P.cm;
   const int64_t max_iter = W.max_iter > 0 ? W.max_iter : 10 * (int64_t)ndof;
+  const bool need_in = W.explicit_rhs || W.x0_mode == 1;
 
   for (int i = c.tid; i < C::VT; i += C::THREADS) Vt[i] = 0.0;
   for (int i = c.tid; i < 6 * C::GL; i += C::THREADS) gens[i] = P.gens[i];
   group_sync<C::G>();
 
   const int cid = blockIdx.x / C::G;
-  double* scr = P.scratch + (size_t)cid * 3 * C::NP * C::NP;
-  double* sx_ = scr;                         // iterate x
-  double* sr_ = scr + C::NP * C::NP;         // residual r
-  double* sb_ = scr + 2 * C::NP * C::NP;     // right-hand side b
+  double* sb_ = P.scratch + (size_t)cid * C::NP * C::NP;  // right-hand side b (true-residual checks only)
   int buf = 0;
 
-  double acc[C::WR][C::NF][4];
+  double acc[C::WR][C::NF][4];  // operator output of the current matvec
+  double rr_[C::WR][C::NF][4];  // CG residual r (register resident)
 
   for (;;) {
     if (c.rank == 0 && c.tid == 0) {
@@ -153,30 +160,28 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
 
     const int n0 = W.first + chain * W.cstride;
     const int n1 = min(n0 + W.clen - 1, W.nmax);
-    bool chain_ok = true;
-    for (int n = n0; n <= n1 && chain_ok; ++n) {
+    bool in_tile = false;  // previous step left this step's input in Vt
+    for (int n = n0; n <= n1; ++n) {
       const double s = 0.5 * W.d_dt[n - 1];
-      const double* in = (n == n0) ? W.d_src + (int64_t)(n - 1) * W.src_stride
-                                   : W.d_out + (int64_t)(n - 1) * W.out_stride;
       const double fs = W.d_f ? (W.d_fscale ? W.d_fscale[n] : 1.0) : 0.0;
       const double* Fn = W.d_f ? W.d_f + (int64_t)n * W.f_stride : nullptr;
-      const bool need_in = W.explicit_rhs || W.x0_mode == 1;
 
       // ---------------- right-hand side, initial iterate and residual --------------
       if (need_in) {
-        load_vec<C>(Vt, in, nx, ny, c);
-        __syncthreads();
+        if (!in_tile) {
+          load_vec<C>(Vt, W.d_src + (int64_t)(n - 1) * W.src_stride, nx, ny, c);
+          __syncthreads();
+        }
         matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true);
       }
+      int64_t nmv = need_in ? 1 : 0;
       double part[2][C::WR][C::WC];
       zero_part<C>(part[0]);
       zero_part<C>(part[1]);
       RM_FOR_ELEM {
         const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
-        const bool ok = j < ny && i < nx;
-        const int si = elem_sidx<C>(c, mr, nf, e);
         double b = 0.0, x = 0.0, r = 0.0;
-        if (ok) {
+        if (j < ny && i < nx) {
           double mv = 0.0, kv = 0.0;
           if (need_in) {
             mv = mass_stencil<C>(Vt, j, i, cm);
@@ -194,31 +199,29 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
             r = b;  // x0 = 0: r = b - A*0 (krylov.py:47,50)
           }
         }
-        sb_[si] = b;
-        sx_[si] = x;
-        sr_[si] = r;
+        sb_[elem_sidx<C>(c, mr, nf, e)] = b;
+        xs[elem_xidx<C>(c, mr, nf, e)] = x;
+        rr_[mr][nf][e] = r;
         part[0][mr][nf >> 1] += b * b;
         part[1][mr][nf >> 1] += r * r;
       }
       if (W.x0_mode == 2) {
         // given initial iterate (spacetime_residual, stepper.py:203)
         __syncthreads();
-        group_sync<C::G>();  // every CTA done with Vt before it is overwritten
         load_vec<C>(Vt, W.d_x0 + (int64_t)n * W.x0_stride, nx, ny, c);
         __syncthreads();
         matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true);
+        ++nmv;
         zero_part<C>(part[1]);
         RM_FOR_ELEM {
           const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
-          const bool ok = j < ny && i < nx;
-          const int si = elem_sidx<C>(c, mr, nf, e);
           double x = 0.0, r = 0.0;
-          if (ok) {
+          if (j < ny && i < nx) {
             x = Vt[vt_idx<C>(j, i)];
-            r = sb_[si] - (mass_stencil<C>(Vt, j, i, cm) + s * acc[mr][nf][e]);
+            r = sb_[elem_sidx<C>(c, mr, nf, e)] - (mass_stencil<C>(Vt, j, i, cm) + s * acc[mr][nf][e]);
           }
-          sx_[si] = x;
-          sr_[si] = r;
+          xs[elem_xidx<C>(c, mr, nf, e)] = x;
+          rr_[mr][nf][e] = r;
           part[1][mr][nf >> 1] += r * r;
         }
       }
@@ -230,19 +233,18 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
       double res = sqrt(tot[1]);
       double rr = tot[1];
       int64_t its = 0;
-      int64_t nmv = (need_in ? 1 : 0) + (W.x0_mode == 2 ? 1 : 0);
       int fail = 0;
       bool done = res <= target;
 
       if (!done) {
-        // p = r into the shared operand tile of every CTA of the group
+        // p = r into the operand tile of every CTA of the group
         RM_FOR_ELEM {
           const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
-          if (j < ny && i < nx) put_elem<C>(vt_peer, vt_idx<C>(j, i), sr_[elem_sidx<C>(c, mr, nf, e)]);
+          if (j < ny && i < nx) put_elem<C>(vt_peer, vt_idx<C>(j, i), rr_[mr][nf][e]);
         }
         group_sync<C::G>();
       }
-      for (int64_t k = 1; !done && !fail; ++k) {
+      for (int64_t k = 1; !done; ++k) {
         if (k > max_iter) {
           fail = RM_CG_BUDGET;
           its = max_iter;
@@ -274,13 +276,11 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
         zero_part<C>(p1[0]);
         RM_FOR_ELEM {
           const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
-          const int si = elem_sidx<C>(c, mr, nf, e);
           if (j < ny && i < nx) {
-            const double pv = Vt[vt_idx<C>(j, i)];
-            const double xn = sx_[si] + alpha * pv;
-            const double rn = sr_[si] - alpha * acc[mr][nf][e];
-            sx_[si] = xn;
-            sr_[si] = rn;
+            const int xi = elem_xidx<C>(c, mr, nf, e);
+            xs[xi] = xs[xi] + alpha * Vt[vt_idx<C>(j, i)];
+            const double rn = rr_[mr][nf][e] - alpha * acc[mr][nf][e];
+            rr_[mr][nf][e] = rn;
             p1[0][mr][nf >> 1] += rn * rn;
           }
         }
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           // acceptance on the true residual (krylov.py:71-83)
           RM_FOR_ELEM {
             const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
-            if (j < ny && i < nx) put_elem<C>(vt_peer, vt_idx<C>(j, i), sx_[elem_sidx<C>(c, mr, nf, e)]);
+            if (j < ny && i < nx) put_elem<C>(vt_peer, vt_idx<C>(j, i), xs[elem_xidx<C>(c, mr, nf, e)]);
           }
           group_sync<C::G>();
           matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true);
@@ -306,9 +306,9 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           zero_part<C>(p1[0]);
           RM_FOR_ELEM {
             const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
-            const int si = elem_sidx<C>(c, mr, nf, e);
             double rt = 0.0;
-            if (j < ny && i < nx) rt = sb_[si] - (mass_stencil<C>(Vt, j, i, cm) + s * acc[mr][nf][e]);
+            if (j < ny && i < nx)
+              rt = sb_[elem_sidx<C>(c, mr, nf, e)] - (mass_stencil<C>(Vt, j, i, cm) + s * acc[mr][nf][e]);
             acc[mr][nf][e] = rt;
             p1[0][mr][nf >> 1] += rt * rt;
           }
@@ -325,11 +325,9 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           rr_new = tt[0];
           res = true_res;
           RM_FOR_ELEM {
+            rr_[mr][nf][e] = acc[mr][nf][e];
             const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
-            if (j < ny && i < nx) {
-              sr_[elem_sidx<C>(c, mr, nf, e)] = acc[mr][nf][e];
-              put_elem<C>(vt_peer, vt_idx<C>(j, i), acc[mr][nf][e]);
-            }
+            if (j < ny && i < nx) put_elem<C>(vt_peer, vt_idx<C>(j, i), acc[mr][nf][e]);
           }
           if (res <= target) {
             its = k;
@@ -346,7 +344,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
           if (j < ny && i < nx) {
             const int vi = vt_idx<C>(j, i);
-            put_elem<C>(vt_peer, vi, sr_[elem_sidx<C>(c, mr, nf, e)] + beta * Vt[vi]);
+            put_elem<C>(vt_peer, vi, rr_[mr][nf][e] + beta * Vt[vi]);
           }
         }
         group_sync<C::G>();
@@ -363,11 +361,13 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           P.fail_info[1] = (double)its;
           P.fail_info[2] = res;
         }
-        chain_ok = false;
-        break;
+        group_sync<C::G>();
+        break;  // abandon the chain (the host raises CgFailure)
       }
 
       // ---------------- MGRIT epilogue: y = [G_n +] x [- S_n] ----------------
+      // every CTA is past its last read of Vt (the final reduction synchronised the group)
+      const bool next_in_tile = n < n1 && need_in;
       const int oi = n / W.out_div;
       const double* Gn = W.d_gadd ? W.d_gadd + (int64_t)n * W.gadd_stride : nullptr;
       const double* Sn = W.d_sub ? W.d_sub + (int64_t)n * W.sub_stride : nullptr;
@@ -378,10 +378,11 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
         const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
         if (j < ny && i < nx) {
           const int gi = j * nx + i;
-          double y = sx_[elem_sidx<C>(c, mr, nf, e)];
+          double y = xs[elem_xidx<C>(c, mr, nf, e)];
           if (Gn) y = __ldcg(Gn + gi) + y;
           if (Sn) y = y - __ldcg(Sn + gi);
           if (On) On[gi] = y;
+          if (next_in_tile) put_elem<C>(vt_peer, vt_idx<C>(j, i), y);
           p1[0][mr][nf >> 1] += y * y;
         }
       }
@@ -391,8 +392,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
         buf ^= 1;
         if (c.rank == 0 && c.tid == 0) W.d_norms[oi] = yy[0];
       }
-      // make y visible to every CTA of the group before the next step loads it
-      __threadfence();
+      in_tile = next_in_tile;
       group_sync<C::G>();
     }
   }
@@ -586,7 +586,6 @@ static cudaError_t max_clusters_t(int* out) {
   X(64, 1)                \
   X(64, 2)                \
   X(64, 4)                \
-  X(128, 1)               \
   X(128, 2)               \
   X(128, 4)               \
   X(128, 8)               \
@@ -628,9 +627,9 @@ template <int NP>
 static cudaError_t launch_apply_t(const ApplyArgs& a, int batch, cudaStream_t st) {
   using C = Cfg<NP, 1>;
   auto kern = apply_kernel<C>;
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::APPLY_SMEM);
   if (err != cudaSuccess) return err;
-  kern<<<batch, C::THREADS, C::SMEM, st>>>(a);
+  kern<<<batch, C::THREADS, C::APPLY_SMEM, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -14,7 +14,7 @@ struct ChainArgs {
   int nx, ny;
   double cm;
   const double* gens;  // 6 generator tables of length 2*NP+8 (device)
-  double* scratch;     // 3*NP*NP doubles per cluster (device)
+  double* scratch;     // NP*NP doubles per cluster (device): right-hand side b
   int* chain_counter;  // work counter, zeroed before launch
   int* fail;           // first-failure flag
   double* fail_info;   // n, iterations, residual norm

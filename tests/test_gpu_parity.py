@@ -285,7 +285,7 @@ def test_results_independent_of_cluster_size(M):
 
 
 def _supported(np_, G):
-    table = {16: (1,), 32: (1, 2), 64: (1, 2, 4), 128: (1, 2, 4, 8, 16)}
+    table = {16: (1,), 32: (1, 2), 64: (1, 2, 4), 128: (2, 4, 8, 16)}
     return G in table[np_]
 
 
