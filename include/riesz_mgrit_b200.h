@@ -144,6 +144,9 @@ RM_API int rm_sweep_run(rm_grid* grid, const rm_sweep* sweep, void* stream);
 RM_API int rm_fail_info(rm_grid* grid, int* code, int* n, int64_t* iterations, double* residual_norm);
 RM_API int rm_fail_reset(rm_grid* grid, void* stream);
 
+/* Debug: per-phase cycle counters of CTA 0 (filled only by -DRM_TIMING builds). */
+RM_API int rm_debug_timing(rm_grid* grid, long long* out16);
+
 /*
  * coarse_correct (mgrit.py:185-189): U[k*m] += Uc[k] for k <= nc.
  */

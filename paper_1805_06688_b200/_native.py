@@ -57,6 +57,7 @@ EXPORTS = {
     "rm_fail_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int64),
                                C.POINTER(C.c_double)]),
     "rm_fail_reset": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "rm_debug_timing": (C.c_int, [C.c_void_p, C.POINTER(C.c_longlong)]),
     "rm_correct": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
                              C.c_void_p]),
     "rm_diff_sqnorm": (C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
@@ -75,9 +76,11 @@ def lib():
         return _lib
     with _lock:
         if _lib is None:
-            path = _build.lib_path()
-            if not os.path.exists(path) or (_build.is_stale() and os.environ.get("RM_NO_BUILD") != "1"):
-                path = _build.build()
+            path = os.environ.get("RM_LIB")  # e.g. the -DRM_TIMING debug variant
+            if not path:
+                path = _build.lib_path()
+                if not os.path.exists(path) or (_build.is_stale() and os.environ.get("RM_NO_BUILD") != "1"):
+                    path = _build.build()
             handle = C.CDLL(path)
             for name, (res, args) in EXPORTS.items():
                 fn = getattr(handle, name)

@@ -54,15 +54,17 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    out = lib_path()
+def build(force: bool = False, verbose: bool = False, timing: bool = False) -> str:
+    """Build the library; ``timing=True`` builds a phase-timing debug variant next to it."""
+    out = lib_path() if not timing else lib_path().replace(".so", "_timing.so")
     if not force and not is_stale():
         return out
     os.makedirs(LIBDIR, exist_ok=True)
     objs = []
     for src in SOURCES:
         obj = os.path.join(LIBDIR, src.replace(".cu", ".o"))
-        cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(REPO, "include"), "-I", CSRC, "-c",
+        extra = ["-DRM_TIMING"] if timing else []
+        cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(REPO, "include"), "-I", CSRC, "-c",
                os.path.join(CSRC, src), "-o", obj]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
@@ -82,4 +84,4 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, timing="--timing" in sys.argv))

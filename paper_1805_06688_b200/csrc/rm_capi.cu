@@ -51,6 +51,7 @@ struct rm_grid {
   int* d_counter = nullptr;
   int* d_fail = nullptr;
   double* d_fail_info = nullptr;
+  long long* d_timing = nullptr;
   int max_clusters[5] = {0, 0, 0, 0, 0};
 };
 
@@ -125,7 +126,9 @@ int rm_grid_create(int nx, int ny, const double* t1x_col, const double* t1x_row,
       (e = cudaMalloc(&g->d_counter, sizeof(int))) != cudaSuccess ||
       (e = cudaMalloc(&g->d_fail, sizeof(int))) != cudaSuccess ||
       (e = cudaMemset(g->d_fail, 0, sizeof(int))) != cudaSuccess ||
-      (e = cudaMalloc(&g->d_fail_info, 4 * sizeof(double))) != cudaSuccess) {
+      (e = cudaMalloc(&g->d_fail_info, 4 * sizeof(double))) != cudaSuccess ||
+      (e = cudaMalloc(&g->d_timing, 16 * sizeof(long long))) != cudaSuccess ||
+      (e = cudaMemset(g->d_timing, 0, 16 * sizeof(long long))) != cudaSuccess) {
     rm_grid_destroy(g);
     return cuda_fail(e, "rm_grid_create");
   }
@@ -140,6 +143,7 @@ int rm_grid_destroy(rm_grid* g) {
   cudaFree(g->d_counter);
   cudaFree(g->d_fail);
   cudaFree(g->d_fail_info);
+  cudaFree(g->d_timing);
   delete g;
   return RM_OK;
 }
@@ -224,6 +228,7 @@ int rm_sweep_run(rm_grid* g, const rm_sweep* sw, void* stream) {
   a.chain_counter = g->d_counter;
   a.fail = g->d_fail;
   a.fail_info = g->d_fail_info;
+  a.timing = g->d_timing;
   RM_CUDA(cudaMemsetAsync(g->d_counter, 0, sizeof(int), st), "rm_sweep_run: counter reset");
   RM_CUDA(rm::launch_chain(g->np, G, a, slots, st), "rm_sweep_run: launch");
   return RM_OK;
@@ -241,6 +246,12 @@ int rm_fail_info(rm_grid* g, int* code, int* n, int64_t* iterations, double* res
   if (iterations) *iterations = (int64_t)info[1];
   if (residual_norm) *residual_norm = info[2];
   return 1;
+}
+
+int rm_debug_timing(rm_grid* g, long long* out16) {
+  if (!g || !out16) return fail(RM_EINVAL, "rm_debug_timing: bad argument");
+  RM_CUDA(cudaMemcpy(out16, g->d_timing, 16 * sizeof(long long), cudaMemcpyDeviceToHost), "rm_debug_timing");
+  return RM_OK;
 }
 
 int rm_fail_reset(rm_grid* g, void* stream) {

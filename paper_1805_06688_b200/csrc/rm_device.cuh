@@ -45,8 +45,9 @@ struct Cfg {
   static constexpr int CR = (G <= UR) ? UR / G : 1;
   static constexpr int CC = (G <= UR) ? UR : UR / (G / UR);
   static constexpr int CU = CR * CC;  // units per CTA
-  static constexpr int WR = CU >= 32 ? 2 : 1;
-  static constexpr int WC = CU >= 64 ? 4 : (CU >= 16 ? 2 : 1);
+  // one warp per 16x16 unit up to 16 warps (4 per SMSP), two units per warp beyond that
+  static constexpr int WR = CU >= 64 ? 2 : 1;
+  static constexpr int WC = CU >= 64 ? 2 : (CU >= 32 ? 2 : 1);
   static constexpr int WARPS = CU / (WR * WC);
   static constexpr int THREADS = WARPS * 32;
   static constexpr int NF = 2 * WC;  // 8-wide n-fragments per warp
@@ -59,7 +60,7 @@ struct Cfg {
   static constexpr size_t APPLY_SMEM = sizeof(double) * (VT + 6 * GL);
   static_assert(G * CU == U, "CTA tiling");
   static_assert(CR % WR == 0 && CC % WC == 0, "warp tiling");
-  static_assert(WARPS >= 1 && WARPS <= 8, "warps");
+  static_assert(WARPS >= 1 && WARPS <= 16, "warps");
 };
 
 __device__ __forceinline__ void dmma(double (&c)[4], double a0, double a1, double b0) {
@@ -162,6 +163,97 @@ __device__ __forceinline__ void group_sync() {
     __syncthreads();
   } else {
     cgx::this_cluster().sync();
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Cluster broadcast of each CTA's region of the operand tile (bulk async copies).
+// Every CTA owns a band of the output units; after it has written its band of
+// Vt it pushes the band into every peer's Vt with cp.async.bulk
+// (shared::cta -> shared::cluster, TMA engine) completing on the peer's
+// mbarrier, then waits on its own mbarrier for the G-1 incoming bands.
+// ----------------------------------------------------------------------------
+template <class C>
+struct Bcast {
+  uint32_t mbar;   // shared::cta address of this CTA's mbarrier
+  uint32_t phase;  // parity of the next phase to wait for
+  uint32_t vt;     // shared::cta address of Vt
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ uint32_t cluster_addr(uint32_t local, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+
+template <class C>
+__device__ __forceinline__ void bcast_setup(Bcast<C>& b, double* Vt, uint64_t* mbar, int tid) {
+  b.mbar = smem_addr(mbar);
+  b.vt = smem_addr(Vt);
+  b.phase = 0;
+  if constexpr (C::G > 1) {
+    if (tid == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b.mbar));
+      asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+  }
+}
+
+// Region of Vt owned by CTA `rank`: nseg segments of seg_bytes starting at seg_off(t).
+template <class C>
+__device__ __forceinline__ uint32_t bcast_seg_off(int rank, int t) {
+  if constexpr (C::G <= C::UR) {
+    return static_cast<uint32_t>(sizeof(double) * (rank * C::CR * 16 + 1) * C::S);
+  } else {
+    constexpr int per = C::G / C::UR;
+    const int r = 16 * (rank / per) + t;
+    const int c0 = (rank % per) * C::CC * 16;
+    return static_cast<uint32_t>(sizeof(double) * ((r + 1) * C::S + c0 + 2));
+  }
+}
+template <class C>
+struct BcastShape {
+  static constexpr int NSEG = (C::G <= C::UR) ? 1 : 16;
+  static constexpr uint32_t SEG_BYTES =
+      (C::G <= C::UR) ? sizeof(double) * C::CR * 16 * C::S : sizeof(double) * C::CC * 16;
+};
+
+// Call after this CTA's threads wrote their elements of Vt (own band only).
+template <class C>
+__device__ __forceinline__ void bcast_band(Bcast<C>& b, int rank, int tid) {
+  if constexpr (C::G == 1) {
+    __syncthreads();
+  } else {
+    using SH = BcastShape<C>;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      const uint32_t incoming = (C::G - 1) * SH::NSEG * SH::SEG_BYTES;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b.mbar), "r"(incoming) : "memory");
+    }
+    if (tid < SH::NSEG) {
+      const uint32_t off = bcast_seg_off<C>(rank, tid);
+#pragma unroll 1
+      for (int q = 0; q < C::G; ++q) {
+        if (q == rank) continue;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                cluster_addr(b.vt + off, q)),
+            "r"(b.vt + off), "r"(SH::SEG_BYTES), "r"(cluster_addr(b.mbar, q))
+            : "memory");
+      }
+    }
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tLAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra LAB_WAIT;\n\t}" ::"r"(b.mbar),
+        "r"(b.phase)
+        : "memory");
+    b.phase ^= 1;
   }
 }
 

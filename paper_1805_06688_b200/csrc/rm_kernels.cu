@@ -20,6 +20,20 @@
 
 namespace rm {
 
+#ifdef RM_TIMING
+// phase timing of CTA 0 (debug builds only: python -m paper_1805_06688_b200.build --timing)
+#define RM_T0() long long t_mark_ = clock64();
+#define RM_T(slot)                                                     \
+  do {                                                                 \
+    long long t_now_ = clock64();                                      \
+    if (blockIdx.x == 0 && threadIdx.x == 0) P.timing[slot] += t_now_ - t_mark_; \
+    t_mark_ = t_now_;                                                  \
+  } while (0)
+#else
+#define RM_T0()
+#define RM_T(slot)
+#endif
+
 // ----------------------------------------------------------------------------
 // chain kernel
 // ----------------------------------------------------------------------------
@@ -59,12 +73,6 @@ __device__ __forceinline__ void load_vec(double* Vt, const double* __restrict__ 
 }
 
 template <class C>
-__device__ __forceinline__ void put_elem(double* const* vt_peer, int idx, double v) {
-#pragma unroll
-  for (int q = 0; q < C::G; ++q) vt_peer[q][idx] = v;
-}
-
-template <class C>
 __device__ __forceinline__ void zero_part(double (&p)[C::WR][C::WC]) {
 #pragma unroll
   for (int mr = 0; mr < C::WR; ++mr)
@@ -86,7 +94,8 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
   double* gens = Vt + C::VT;           // generator tables
   double* red = gens + 6 * C::GL;      // reduction buffers
   double* xs = red + C::RED;           // this CTA's part of the CG iterate x
-  int* sched = reinterpret_cast<int*>(xs + C::XS);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(xs + C::XS);
+  int* sched = reinterpret_cast<int*>(mbar + 1);
 
   Ctx<C> c;
   c.tid = threadIdx.x;
@@ -111,18 +120,15 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
     c.ucol = c0 + (c.warp % wcols) * C::WC;
   }
 
-  double* vt_peer[C::G];
   double* red_peer[C::G];
   int* sched_peer[C::G];
   if constexpr (C::G == 1) {
-    vt_peer[0] = Vt;
     red_peer[0] = red;
     sched_peer[0] = sched;
   } else {
     auto cl = cgx::this_cluster();
 #pragma unroll
     for (int q = 0; q < C::G; ++q) {
-      vt_peer[q] = cl.map_shared_rank(Vt, q);
       red_peer[q] = cl.map_shared_rank(red, q);
       sched_peer[q] = cl.map_shared_rank(sched, q);
     }
@@ -138,6 +144,8 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
 
   for (int i = c.tid; i < C::VT; i += C::THREADS) Vt[i] = 0.0;
   for (int i = c.tid; i < 6 * C::GL; i += C::THREADS) gens[i] = P.gens[i];
+  Bcast<C> bc;
+  bcast_setup<C>(bc, Vt, mbar, c.tid);
   group_sync<C::G>();
 
   const int cid = blockIdx.x / C::G;
@@ -240,19 +248,22 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
         // p = r into the operand tile of every CTA of the group
         RM_FOR_ELEM {
           const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
-          if (j < ny && i < nx) put_elem<C>(vt_peer, vt_idx<C>(j, i), rr_[mr][nf][e]);
+          if (j < ny && i < nx) Vt[vt_idx<C>(j, i)] = rr_[mr][nf][e];
         }
-        group_sync<C::G>();
+        bcast_band<C>(bc, c.rank, c.tid);
       }
+      RM_T0();
       for (int64_t k = 1; !done; ++k) {
         if (k > max_iter) {
           fail = RM_CG_BUDGET;
           its = max_iter;
           break;
         }
+        RM_T(7);
         // Ap and p'Ap
         matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true);
         ++nmv;
+        RM_T(0);
         double p1[1][C::WR][C::WC];
         zero_part<C>(p1[0]);
         RM_FOR_ELEM {
@@ -264,9 +275,11 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           }
           acc[mr][nf][e] = ap;
         }
+        RM_T(1);
         double pap[1];
         group_reduce<C, 1>(p1, red, red_peer, buf, c.urow, c.ucol, c.lane, pap);
         buf ^= 1;
+        RM_T(2);
         if (!isfinite(pap[0]) || pap[0] <= 0.0) {
           fail = RM_CG_BREAKDOWN;
           its = k;
@@ -284,9 +297,11 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
             p1[0][mr][nf >> 1] += rn * rn;
           }
         }
+        RM_T(3);
         double rrn[1];
         group_reduce<C, 1>(p1, red, red_peer, buf, c.urow, c.ucol, c.lane, rrn);
         buf ^= 1;
+        RM_T(4);
         double rr_new = rrn[0];
         res = sqrt(rr_new);
         if (!isfinite(res)) {
@@ -298,9 +313,9 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           // acceptance on the true residual (krylov.py:71-83)
           RM_FOR_ELEM {
             const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
-            if (j < ny && i < nx) put_elem<C>(vt_peer, vt_idx<C>(j, i), xs[elem_xidx<C>(c, mr, nf, e)]);
+            if (j < ny && i < nx) Vt[vt_idx<C>(j, i)] = xs[elem_xidx<C>(c, mr, nf, e)];
           }
-          group_sync<C::G>();
+          bcast_band<C>(bc, c.rank, c.tid);
           matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true);
           ++nmv;
           zero_part<C>(p1[0]);
@@ -327,15 +342,15 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           RM_FOR_ELEM {
             rr_[mr][nf][e] = acc[mr][nf][e];
             const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
-            if (j < ny && i < nx) put_elem<C>(vt_peer, vt_idx<C>(j, i), acc[mr][nf][e]);
+            if (j < ny && i < nx) Vt[vt_idx<C>(j, i)] = acc[mr][nf][e];
           }
+          bcast_band<C>(bc, c.rank, c.tid);
           if (res <= target) {
             its = k;
             done = true;
             break;
           }
           rr = rr_new;
-          group_sync<C::G>();
           continue;
         }
         const double beta = rr_new / rr;
@@ -344,10 +359,12 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
           if (j < ny && i < nx) {
             const int vi = vt_idx<C>(j, i);
-            put_elem<C>(vt_peer, vi, rr_[mr][nf][e] + beta * Vt[vi]);
+            Vt[vi] = rr_[mr][nf][e] + beta * Vt[vi];
           }
         }
-        group_sync<C::G>();
+        RM_T(5);
+        bcast_band<C>(bc, c.rank, c.tid);
+        RM_T(6);
       }
 
       if (c.rank == 0 && c.tid == 0) {
@@ -382,7 +399,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           if (Gn) y = __ldcg(Gn + gi) + y;
           if (Sn) y = y - __ldcg(Sn + gi);
           if (On) On[gi] = y;
-          if (next_in_tile) put_elem<C>(vt_peer, vt_idx<C>(j, i), y);
+          if (next_in_tile) Vt[vt_idx<C>(j, i)] = y;
           p1[0][mr][nf >> 1] += y * y;
         }
       }
@@ -393,6 +410,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
         if (c.rank == 0 && c.tid == 0) W.d_norms[oi] = yy[0];
       }
       in_tile = next_in_tile;
+      if (next_in_tile) bcast_band<C>(bc, c.rank, c.tid);
       group_sync<C::G>();
     }
   }

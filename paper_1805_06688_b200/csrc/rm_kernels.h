@@ -18,6 +18,7 @@ struct ChainArgs {
   int* chain_counter;  // work counter, zeroed before launch
   int* fail;           // first-failure flag
   double* fail_info;   // n, iterations, residual norm
+  long long* timing;   // RM_TIMING builds: per-phase cycles of CTA 0
 };
 
 struct ApplyArgs {
