@@ -131,10 +131,20 @@ typedef struct rm_sweep {
   double rel_tol;
   int64_t max_iter; /* <= 0: 10*ndof (CgOptions default, krylov.py:12-20) */
   unsigned long long* d_counters;
-  int group; /* CTAs per chain (cluster size); 0 = library choice */
+  int group;   /* CTAs per chain (cluster size); 0 = library choice */
+  int precond; /* 0: plain CG (the reference algorithm); 1: tau-preconditioned CG (needs
+                  rm_grid_set_tau); both stop on ||b - A x|| <= rel_tol ||b|| */
 } rm_sweep;
 
 RM_API int rm_sweep_run(rm_grid* grid, const rm_sweep* sweep, void* stream);
+
+/*
+ * Install the tau (sine-transform) preconditioner: P(s) = (S_y (x) S_x) diag(dm + s*dk) (S_y (x) S_x)
+ * with S the orthonormal DST-I matrices; dm, dk are host arrays [ny*nx] (x fastest), the diagonal of
+ * the mass and stiffness parts of (S(x)S) A (S(x)S) (paper_1805_06688_b200/precond.py).  Extension of
+ * cg_solve (krylov.py:32-92): same stopping rule, fewer iterations.
+ */
+RM_API int rm_grid_set_tau(rm_grid* grid, const double* dm, const double* dk);
 
 /*
  * First CG failure since the last rm_fail_reset: returns 1 and fills

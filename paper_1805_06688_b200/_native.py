@@ -40,6 +40,7 @@ class Sweep(C.Structure):
         ("max_iter", C.c_int64),
         ("d_counters", C.c_void_p),
         ("group", C.c_int),
+        ("precond", C.c_int),
     ]
 
 
@@ -54,6 +55,7 @@ EXPORTS = {
     "rm_apply_batched": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int64,
                                    C.c_void_p, C.c_int64, C.c_void_p]),
     "rm_sweep_run": (C.c_int, [C.c_void_p, C.POINTER(Sweep), C.c_void_p]),
+    "rm_grid_set_tau": (C.c_int, [C.c_void_p, _D, _D]),
     "rm_fail_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int64),
                                C.POINTER(C.c_double)]),
     "rm_fail_reset": (C.c_int, [C.c_void_p, C.c_void_p]),

@@ -317,7 +317,7 @@ def device_implicit_solve(engine, dt: float, b: torch.Tensor, x0, opts: CgOption
         kw = dict(x0_mode=0)
     engine.sweep(nchains=B, first=1, cstride=1, clen=1, nmax=B, dt=dts, counters=counters,
                  rel_tol=opts.rel_tol, max_iter=opts.max_iter, explicit=False, f=(b, -1), f_stride=engine.ndof,
-                 out=(out, -1), group=group, **kw)
+                 out=(out, -1), group=group, precond=opts.preconditioner, **kw)
     engine.check_fail()
     return out
 

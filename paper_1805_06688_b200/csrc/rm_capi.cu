@@ -52,6 +52,9 @@ struct rm_grid {
   int* d_fail = nullptr;
   double* d_fail_info = nullptr;
   long long* d_timing = nullptr;
+  double* d_dm = nullptr;  // tau preconditioner (rm_grid_set_tau)
+  double* d_dk = nullptr;
+  double* d_tab = nullptr;  // sine tables x then y
   int max_clusters[5] = {0, 0, 0, 0, 0};
 };
 
@@ -122,7 +125,7 @@ int rm_grid_create(int nx, int ny, const double* t1x_col, const double* t1x_row,
   g->scratch_clusters = maxc;
   if ((e = cudaMalloc(&g->d_gens, sizeof(double) * tab.size())) != cudaSuccess ||
       (e = cudaMemcpy(g->d_gens, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice)) != cudaSuccess ||
-      (e = cudaMalloc(&g->d_scratch, sizeof(double) * (size_t)np * np * maxc)) != cudaSuccess ||
+      (e = cudaMalloc(&g->d_scratch, sizeof(double) * 3 * (size_t)np * np * maxc)) != cudaSuccess ||
       (e = cudaMalloc(&g->d_counter, sizeof(int))) != cudaSuccess ||
       (e = cudaMalloc(&g->d_fail, sizeof(int))) != cudaSuccess ||
       (e = cudaMemset(g->d_fail, 0, sizeof(int))) != cudaSuccess ||
@@ -144,6 +147,9 @@ int rm_grid_destroy(rm_grid* g) {
   cudaFree(g->d_fail);
   cudaFree(g->d_fail_info);
   cudaFree(g->d_timing);
+  cudaFree(g->d_dm);
+  cudaFree(g->d_dk);
+  cudaFree(g->d_tab);
   delete g;
   return RM_OK;
 }
@@ -208,6 +214,7 @@ int rm_sweep_run(rm_grid* g, const rm_sweep* sw, void* stream) {
     return fail(RM_EINVAL, "rm_sweep_run: chains longer than one step need d_out with out_div == 1");
   if (!sw->d_counters) return fail(RM_EINVAL, "rm_sweep_run: d_counters is required");
   if (!(sw->rel_tol > 0)) return fail(RM_EINVAL, "relative tolerance must be positive");
+  if (sw->precond && !g->d_dm) return fail(RM_EINVAL, "rm_sweep_run: precond=1 needs rm_grid_set_tau first");
   int G = sw->group > 0 ? sw->group : choose_group(g, sw->nchains);
   if (!rm::chain_supported(g->np, G))
     return fail(RM_EUNSUP, "rm_sweep_run: group size " + std::to_string(G) + " unsupported for order " +
@@ -229,8 +236,37 @@ int rm_sweep_run(rm_grid* g, const rm_sweep* sw, void* stream) {
   a.fail = g->d_fail;
   a.fail_info = g->d_fail_info;
   a.timing = g->d_timing;
+  a.dm = g->d_dm;
+  a.dk = g->d_dk;
+  a.tabx = g->d_tab;
+  a.taby = g->d_tab ? g->d_tab + (2 * g->np + 8) : nullptr;
   RM_CUDA(cudaMemsetAsync(g->d_counter, 0, sizeof(int), st), "rm_sweep_run: counter reset");
   RM_CUDA(rm::launch_chain(g->np, G, a, slots, st), "rm_sweep_run: launch");
+  return RM_OK;
+}
+
+int rm_grid_set_tau(rm_grid* g, const double* dm, const double* dk) {
+  if (!g || !dm || !dk) return fail(RM_EINVAL, "rm_grid_set_tau: null argument");
+  const size_t n = (size_t)g->nx * g->ny;
+  for (size_t i = 0; i < n; ++i)
+    if (!(dm[i] > 0.0) || !(dk[i] >= 0.0 || dk[i] < 0.0))
+      return fail(RM_EINVAL, "rm_grid_set_tau: the mass diagonal must be positive and finite");
+  const int np = g->np, st = 2 * np + 8;
+  std::vector<double> tab(2 * (size_t)st, 0.0);
+  const int ns[2] = {g->nx, g->ny};
+  for (int t = 0; t < 2; ++t) {
+    const int nn = ns[t], L = 2 * (nn + 1);
+    const double c = sqrt(2.0 / (nn + 1));
+    for (int m = 0; m < L; ++m) tab[t * st + m] = c * sin(M_PI * (double)m / (double)(nn + 1));
+  }
+  cudaError_t e;
+  if (!g->d_dm && ((e = cudaMalloc(&g->d_dm, n * sizeof(double))) != cudaSuccess ||
+                   (e = cudaMalloc(&g->d_dk, n * sizeof(double))) != cudaSuccess ||
+                   (e = cudaMalloc(&g->d_tab, tab.size() * sizeof(double))) != cudaSuccess))
+    return cuda_fail(e, "rm_grid_set_tau");
+  RM_CUDA(cudaMemcpy(g->d_dm, dm, n * sizeof(double), cudaMemcpyHostToDevice), "rm_grid_set_tau");
+  RM_CUDA(cudaMemcpy(g->d_dk, dk, n * sizeof(double), cudaMemcpyHostToDevice), "rm_grid_set_tau");
+  RM_CUDA(cudaMemcpy(g->d_tab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice), "rm_grid_set_tau");
   return RM_OK;
 }
 

@@ -45,9 +45,9 @@ struct Cfg {
   static constexpr int CR = (G <= UR) ? UR / G : 1;
   static constexpr int CC = (G <= UR) ? UR : UR / (G / UR);
   static constexpr int CU = CR * CC;  // units per CTA
-  // one warp per 16x16 unit up to 16 warps (4 per SMSP), two units per warp beyond that
+  // one warp per 16x16 unit up to 16 units per CTA; beyond, 8 warps each owning a 1 x 4 (or 2 x 4) strip
   static constexpr int WR = CU >= 64 ? 2 : 1;
-  static constexpr int WC = CU >= 64 ? 2 : (CU >= 32 ? 2 : 1);
+  static constexpr int WC = CU >= 32 ? 4 : 1;
   static constexpr int WARPS = CU / (WR * WC);
   static constexpr int THREADS = WARPS * 32;
   static constexpr int NF = 2 * WC;  // 8-wide n-fragments per warp
@@ -56,7 +56,8 @@ struct Cfg {
   static constexpr int GL = 2 * NP + 8;  // generator table length
   static constexpr int RED = 2 * 4 * U;  // two reduction buffers of up to 4 values per unit
   static constexpr int XS = CU * 256;    // CG iterate of this CTA's units (shared-memory resident)
-  static constexpr size_t SMEM = sizeof(double) * (VT + 6 * GL + RED + XS) + 64;
+  static constexpr int ST = 2 * NP + 8;  // sine table length (>= 2(n+1))
+  static constexpr size_t SMEM = sizeof(double) * (VT + 6 * GL + RED + XS + 2 * ST) + 64;
   static constexpr size_t APPLY_SMEM = sizeof(double) * (VT + 6 * GL);
   static_assert(G * CU == U, "CTA tiling");
   static_assert(CR % WR == 0 && CC % WC == 0, "warp tiling");
@@ -133,6 +134,69 @@ __device__ __forceinline__ void matvec(const double* __restrict__ Vt, const doub
           for (int nf = 0; nf < C::NF; ++nf) dmma(acc[mr][nf], a[mr][0], a[mr][1], b[nf]);
       }
     }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Dense DST-I contractions for the tau preconditioner, S[a][b] = sqrt(2/(n+1)) sin(pi (a+1)(b+1)/(n+1)),
+// read from a sine table tab[m] (m < L = 2(n+1)) as the A operand of the MMA.
+// dst_y  (normal mapping):     out[j][i] = sum_l Sy[j][l] V[l][i]            (rows of the own units)
+// dst_xT (transposed mapping): out[j][i] = sum_k V[j][k] Sx[k][i], computed as
+//        out^T[i][j] = sum_k Sx[i][k] V^T[k][j] so that the table is again the A operand; the
+//        warp tile is (16 i) x (16*WC j) with j in the CTA's own band.
+// ----------------------------------------------------------------------------
+template <class C>
+__device__ __forceinline__ void dst_y(const double* __restrict__ Vt, const double* __restrict__ tab, int L,
+                                      double (&acc)[C::WR][C::NF][4], int urow, int ucol, int gq, int tig,
+                                      int k_end) {
+  static_assert(C::WR == 1, "DST stages assume one unit row per warp");
+#pragma unroll
+  for (int nf = 0; nf < C::NF; ++nf)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[0][nf][e] = 0.0;
+  const int ja = 16 * urow + gq + 1, jb = ja + 8;
+  int ia = (ja * (tig + 1)) % L, ib = (jb * (tig + 1)) % L;
+  const int sa = (4 * ja) % L, sb = (4 * jb) % L;
+  const double* br = Vt + vt_idx<C>(tig, 16 * ucol + gq);
+#pragma unroll 4
+  for (int l0 = 0; l0 < k_end; l0 += 4) {
+    const double a0 = tab[ia], a1 = tab[ib];
+    double b[C::NF];
+#pragma unroll
+    for (int nf = 0; nf < C::NF; ++nf) b[nf] = br[l0 * C::S + 8 * nf];
+#pragma unroll
+    for (int nf = 0; nf < C::NF; ++nf) dmma(acc[0][nf], a0, a1, b[nf]);
+    ia += sa;
+    ia -= ia >= L ? L : 0;
+    ib += sb;
+    ib -= ib >= L ? L : 0;
+  }
+}
+
+template <class C>
+__device__ __forceinline__ void dst_xT(const double* __restrict__ Vt, const double* __restrict__ tab, int L,
+                                       double (&acc)[C::WR][C::NF][4], int tm, int tn, int gq, int tig,
+                                       int k_end) {
+#pragma unroll
+  for (int nf = 0; nf < C::NF; ++nf)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[0][nf][e] = 0.0;
+  const int xa = 16 * tm + gq + 1, xb = xa + 8;
+  int ia = (xa * (tig + 1)) % L, ib = (xb * (tig + 1)) % L;
+  const int sa = (4 * xa) % L, sb = (4 * xb) % L;
+  const double* br = Vt + vt_idx<C>(16 * tn + gq, tig);
+#pragma unroll 4
+  for (int k0 = 0; k0 < k_end; k0 += 4) {
+    const double a0 = tab[ia], a1 = tab[ib];
+    double b[C::NF];
+#pragma unroll
+    for (int nf = 0; nf < C::NF; ++nf) b[nf] = br[8 * nf * C::S + k0];
+#pragma unroll
+    for (int nf = 0; nf < C::NF; ++nf) dmma(acc[0][nf], a0, a1, b[nf]);
+    ia += sa;
+    ia -= ia >= L ? L : 0;
+    ib += sb;
+    ib -= ib >= L ? L : 0;
   }
 }
 

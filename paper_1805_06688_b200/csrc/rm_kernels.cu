@@ -42,6 +42,7 @@ template <class C>
 struct Ctx {
   int tid, lane, warp, gq, tig, rank;
   int urow, ucol;  // first unit (row, col) of this warp
+  int tm, tn;      // transposed DST stage: unit column (m) and first unit row (n) of this warp
 };
 
 #define RM_FOR_ELEM                                \
@@ -86,16 +87,92 @@ __device__ __forceinline__ int elem_xidx(const Ctx<C>& c, int mr, int nf, int e)
   return (((c.warp * C::WR + mr) * C::WC + (nf >> 1)) * 8 + (nf & 1) * 4 + e) * 32 + c.lane;
 }
 
+// element (row j, col i) held by (nf, e) of the transposed DST-x stage
 template <class C>
+__device__ __forceinline__ int elemT_row(const Ctx<C>& c, int nf, int e) {
+  return 16 * c.tn + 8 * nf + 2 * c.tig + (e & 1);
+}
+template <class C>
+__device__ __forceinline__ int elemT_col(const Ctx<C>& c, int e) {
+  return 16 * c.tm + c.gq + 8 * (e >> 1);
+}
+
+// Shared state of one chain kernel instance (per CTA).
+template <class C>
+struct Smem {
+  double* Vt;
+  double* gens;
+  double* red;
+  double* xs;
+  double* tabx;
+  double* taby;
+  double* red_peer[C::G];
+};
+
+// z = P^{-1} r for the tau preconditioner: Vt <- r; T1 = R Sx; T2 = Sy T1 * dinv; T3 = T2 Sx; z = Sy T3.
+// Precondition: every CTA of the group finished reading Vt.  Result z in acc (normal mapping).
+template <class C>
+__device__ __forceinline__ void apply_tau(const Ctx<C>& c, const Smem<C>& sm, Bcast<C>& bc,
+                                          const double (&r)[C::WR][C::NF][4], double (&acc)[C::WR][C::NF][4],
+                                          const double* __restrict__ dinv, int nx, int ny, int Lx, int Ly,
+                                          long long* timing) {
+  const int kx_end = (nx + 3) & ~3, ky_end = (ny + 3) & ~3;
+  double* Vt = sm.Vt;
+#ifdef RM_TIMING
+  struct {
+    long long* timing;
+  } P{timing};
+#endif
+  RM_T0();
+  RM_FOR_ELEM {
+    const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
+    if (j < ny && i < nx) Vt[vt_idx<C>(j, i)] = r[mr][nf][e];
+  }
+  bcast_band<C>(bc, c.rank, c.tid);
+  RM_T(8);
+#pragma unroll 1
+  for (int pass = 0; pass < 2; ++pass) {
+    // x-direction (transposed mapping)
+    dst_xT<C>(Vt, sm.tabx, Lx, acc, c.tm, c.tn, c.gq, c.tig, kx_end);
+    RM_T(9);
+    group_sync<C::G>();
+    RM_FOR_ELEM {
+      const int j = elemT_row<C>(c, nf, e), i = elemT_col<C>(c, e);
+      if (j < ny && i < nx) Vt[vt_idx<C>(j, i)] = acc[mr][nf][e];
+    }
+    bcast_band<C>(bc, c.rank, c.tid);
+    RM_T(10);
+    // y-direction (normal mapping)
+    dst_y<C>(Vt, sm.taby, Ly, acc, c.urow, c.ucol, c.gq, c.tig, ky_end);
+    RM_T(11);
+    if (pass == 1) break;
+    group_sync<C::G>();
+    RM_FOR_ELEM {
+      const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
+      if (j < ny && i < nx) Vt[vt_idx<C>(j, i)] = acc[mr][nf][e] * __ldcg(dinv + elem_sidx<C>(c, mr, nf, e));
+    }
+    bcast_band<C>(bc, c.rank, c.tid);
+    RM_T(12);
+  }
+}
+
+template <class C, bool PRE>
 __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P) {
   static_assert(C::SMEM <= 227 * 1024, "shared memory budget");
   extern __shared__ __align__(16) double smem[];
-  double* Vt = smem;                   // operand tile (p, or the vector being applied)
-  double* gens = Vt + C::VT;           // generator tables
-  double* red = gens + 6 * C::GL;      // reduction buffers
-  double* xs = red + C::RED;           // this CTA's part of the CG iterate x
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(xs + C::XS);
+  Smem<C> sm;
+  sm.Vt = smem;                    // operand tile (p, or the vector being applied)
+  sm.gens = sm.Vt + C::VT;         // generator tables
+  sm.red = sm.gens + 6 * C::GL;    // reduction buffers
+  sm.xs = sm.red + C::RED;         // this CTA's part of the CG iterate x
+  sm.tabx = sm.xs + C::XS;         // DST sine tables
+  sm.taby = sm.tabx + C::ST;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(sm.taby + C::ST);
   int* sched = reinterpret_cast<int*>(mbar + 1);
+  double* Vt = sm.Vt;
+  double* gens = sm.gens;
+  double* red = sm.red;
+  double* xs = sm.xs;
 
   Ctx<C> c;
   c.tid = threadIdx.x;
@@ -118,18 +195,21 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
     constexpr int wcols = C::CC / C::WC;
     c.urow = r0 + (c.warp / wcols) * C::WR;
     c.ucol = c0 + (c.warp % wcols) * C::WC;
+    // transposed DST stage: m over the CTA's CC unit columns, n over its CR unit rows
+    constexpr int tcols = C::CR / C::WC > 0 ? C::CR / C::WC : 1;
+    c.tm = c0 + c.warp / tcols;
+    c.tn = r0 + (c.warp % tcols) * C::WC;
   }
 
-  double* red_peer[C::G];
   int* sched_peer[C::G];
   if constexpr (C::G == 1) {
-    red_peer[0] = red;
+    sm.red_peer[0] = red;
     sched_peer[0] = sched;
   } else {
     auto cl = cgx::this_cluster();
 #pragma unroll
     for (int q = 0; q < C::G; ++q) {
-      red_peer[q] = cl.map_shared_rank(red, q);
+      sm.red_peer[q] = cl.map_shared_rank(red, q);
       sched_peer[q] = cl.map_shared_rank(sched, q);
     }
   }
@@ -138,21 +218,28 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
   const int nx = P.nx, ny = P.ny;
   const int ndof = nx * ny;
   const int kx_end = (nx + 3) & ~3, ky_end = (ny + 3) & ~3;
+  const int Lx = 2 * (nx + 1), Ly = 2 * (ny + 1);
   const double cm = P.cm;
   const int64_t max_iter = W.max_iter > 0 ? W.max_iter : 10 * (int64_t)ndof;
   const bool need_in = W.explicit_rhs || W.x0_mode == 1;
 
   for (int i = c.tid; i < C::VT; i += C::THREADS) Vt[i] = 0.0;
   for (int i = c.tid; i < 6 * C::GL; i += C::THREADS) gens[i] = P.gens[i];
+  if constexpr (PRE) {
+    for (int i = c.tid; i < Lx; i += C::THREADS) sm.tabx[i] = P.tabx[i];
+    for (int i = c.tid; i < Ly; i += C::THREADS) sm.taby[i] = P.taby[i];
+  }
   Bcast<C> bc;
   bcast_setup<C>(bc, Vt, mbar, c.tid);
   group_sync<C::G>();
 
   const int cid = blockIdx.x / C::G;
-  double* sb_ = P.scratch + (size_t)cid * C::NP * C::NP;  // right-hand side b (true-residual checks only)
+  double* sb_ = P.scratch + (size_t)cid * 3 * C::NP * C::NP;  // right-hand side b (true-residual checks)
+  double* dinv = sb_ + C::NP * C::NP;                         // 1 / d(s) of the tau preconditioner
+  double* pold_ = dinv + C::NP * C::NP;                       // previous search direction (PCG)
   int buf = 0;
 
-  double acc[C::WR][C::NF][4];  // operator output of the current matvec
+  double acc[C::WR][C::NF][4];  // operator output of the current matvec / DST stage
   double rr_[C::WR][C::NF][4];  // CG residual r (register resident)
 
   for (;;) {
@@ -189,6 +276,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
       RM_FOR_ELEM {
         const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
         double b = 0.0, x = 0.0, r = 0.0;
+        const int si = elem_sidx<C>(c, mr, nf, e);
         if (j < ny && i < nx) {
           double mv = 0.0, kv = 0.0;
           if (need_in) {
@@ -206,8 +294,9 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           } else {
             r = b;  // x0 = 0: r = b - A*0 (krylov.py:47,50)
           }
+          if constexpr (PRE) dinv[si] = 1.0 / (__ldg(P.dm + j * nx + i) + s * __ldg(P.dk + j * nx + i));
         }
-        sb_[elem_sidx<C>(c, mr, nf, e)] = b;
+        sb_[si] = b;
         xs[elem_xidx<C>(c, mr, nf, e)] = x;
         rr_[mr][nf][e] = r;
         part[0][mr][nf >> 1] += b * b;
@@ -234,21 +323,37 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
         }
       }
       double tot[2];
-      group_reduce<C, 2>(part, red, red_peer, buf, c.urow, c.ucol, c.lane, tot);
+      group_reduce<C, 2>(part, red, sm.red_peer, buf, c.urow, c.ucol, c.lane, tot);
       buf ^= 1;
       const double bnorm = sqrt(tot[0]);
       const double target = bnorm > 0.0 ? W.rel_tol * bnorm : W.rel_tol;
       double res = sqrt(tot[1]);
-      double rr = tot[1];
+      double rr = tot[1];  // r.r (CG) or r.z (PCG)
       int64_t its = 0;
       int fail = 0;
       bool done = res <= target;
 
       if (!done) {
-        // p = r into the operand tile of every CTA of the group
-        RM_FOR_ELEM {
-          const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
-          if (j < ny && i < nx) Vt[vt_idx<C>(j, i)] = rr_[mr][nf][e];
+        if constexpr (PRE) {
+          // z = P^-1 r, p = z, rz = r.z
+          apply_tau<C>(c, sm, bc, rr_, acc, dinv, nx, ny, Lx, Ly, P.timing);
+          double p1[1][C::WR][C::WC];
+          zero_part<C>(p1[0]);
+          RM_FOR_ELEM { p1[0][mr][nf >> 1] += rr_[mr][nf][e] * acc[mr][nf][e]; }
+          double rz[1];
+          group_reduce<C, 1>(p1, red, sm.red_peer, buf, c.urow, c.ucol, c.lane, rz);
+          buf ^= 1;
+          rr = rz[0];
+          RM_FOR_ELEM {
+            const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
+            if (j < ny && i < nx) Vt[vt_idx<C>(j, i)] = acc[mr][nf][e];
+          }
+        } else {
+          // p = r into the operand tile of every CTA of the group
+          RM_FOR_ELEM {
+            const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
+            if (j < ny && i < nx) Vt[vt_idx<C>(j, i)] = rr_[mr][nf][e];
+          }
         }
         bcast_band<C>(bc, c.rank, c.tid);
       }
@@ -277,7 +382,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
         }
         RM_T(1);
         double pap[1];
-        group_reduce<C, 1>(p1, red, red_peer, buf, c.urow, c.ucol, c.lane, pap);
+        group_reduce<C, 1>(p1, red, sm.red_peer, buf, c.urow, c.ucol, c.lane, pap);
         buf ^= 1;
         RM_T(2);
         if (!isfinite(pap[0]) || pap[0] <= 0.0) {
@@ -286,23 +391,44 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           break;
         }
         const double alpha = rr / pap[0];
-        zero_part<C>(p1[0]);
+        double part2[2][C::WR][C::WC];
+        zero_part<C>(part2[0]);
+        zero_part<C>(part2[1]);
         RM_FOR_ELEM {
           const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
           if (j < ny && i < nx) {
             const int xi = elem_xidx<C>(c, mr, nf, e);
-            xs[xi] = xs[xi] + alpha * Vt[vt_idx<C>(j, i)];
+            const double pv = Vt[vt_idx<C>(j, i)];
+            xs[xi] = xs[xi] + alpha * pv;
             const double rn = rr_[mr][nf][e] - alpha * acc[mr][nf][e];
             rr_[mr][nf][e] = rn;
-            p1[0][mr][nf >> 1] += rn * rn;
+            part2[0][mr][nf >> 1] += rn * rn;
+            // the preconditioner overwrites the operand tile: keep p for the direction update
+            if constexpr (PRE) pold_[elem_sidx<C>(c, mr, nf, e)] = pv;
           }
         }
         RM_T(3);
-        double rrn[1];
-        group_reduce<C, 1>(p1, red, red_peer, buf, c.urow, c.ucol, c.lane, rrn);
+        double red2[2];
+        if constexpr (PRE) {
+          // z = P^-1 r; reduce r.r (convergence test) and r.z together
+          apply_tau<C>(c, sm, bc, rr_, acc, dinv, nx, ny, Lx, Ly, P.timing);
+          RM_T0();
+          RM_FOR_ELEM { part2[1][mr][nf >> 1] += rr_[mr][nf][e] * acc[mr][nf][e]; }
+          group_reduce<C, 2>(part2, red, sm.red_peer, buf, c.urow, c.ucol, c.lane, red2);
+        } else {
+          double p0[1][C::WR][C::WC];
+#pragma unroll
+          for (int mr = 0; mr < C::WR; ++mr)
+#pragma unroll
+            for (int uc = 0; uc < C::WC; ++uc) p0[0][mr][uc] = part2[0][mr][uc];
+          double one[1];
+          group_reduce<C, 1>(p0, red, sm.red_peer, buf, c.urow, c.ucol, c.lane, one);
+          red2[0] = one[0];
+          red2[1] = one[0];
+        }
         buf ^= 1;
         RM_T(4);
-        double rr_new = rrn[0];
+        double rr_new = red2[0];
         res = sqrt(rr_new);
         if (!isfinite(res)) {
           fail = RM_CG_NONFINITE;
@@ -328,7 +454,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
             p1[0][mr][nf >> 1] += rt * rt;
           }
           double tt[1];
-          group_reduce<C, 1>(p1, red, red_peer, buf, c.urow, c.ucol, c.lane, tt);
+          group_reduce<C, 1>(p1, red, sm.red_peer, buf, c.urow, c.ucol, c.lane, tt);
           buf ^= 1;
           const double true_res = sqrt(tt[0]);
           if (true_res <= fmax(target, 10.0 * res)) {
@@ -337,29 +463,42 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
             break;
           }
           // recurrence drifted: restart from the true residual
-          rr_new = tt[0];
           res = true_res;
-          RM_FOR_ELEM {
-            rr_[mr][nf][e] = acc[mr][nf][e];
-            const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
-            if (j < ny && i < nx) Vt[vt_idx<C>(j, i)] = acc[mr][nf][e];
-          }
-          bcast_band<C>(bc, c.rank, c.tid);
+          RM_FOR_ELEM { rr_[mr][nf][e] = acc[mr][nf][e]; }
           if (res <= target) {
             its = k;
             done = true;
             break;
           }
-          rr = rr_new;
+          if constexpr (PRE) {
+            apply_tau<C>(c, sm, bc, rr_, acc, dinv, nx, ny, Lx, Ly, P.timing);
+            zero_part<C>(p1[0]);
+            RM_FOR_ELEM { p1[0][mr][nf >> 1] += rr_[mr][nf][e] * acc[mr][nf][e]; }
+            double rz[1];
+            group_reduce<C, 1>(p1, red, sm.red_peer, buf, c.urow, c.ucol, c.lane, rz);
+            buf ^= 1;
+            rr = rz[0];
+          } else {
+            rr = tt[0];
+          }
+          RM_FOR_ELEM {
+            const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
+            if (j < ny && i < nx) Vt[vt_idx<C>(j, i)] = acc[mr][nf][e];
+          }
+          bcast_band<C>(bc, c.rank, c.tid);
           continue;
         }
-        const double beta = rr_new / rr;
-        rr = rr_new;
+        const double rho_new = red2[1];
+        const double beta = rho_new / rr;
+        rr = rho_new;
         RM_FOR_ELEM {
           const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
           if (j < ny && i < nx) {
             const int vi = vt_idx<C>(j, i);
-            Vt[vi] = rr_[mr][nf][e] + beta * Vt[vi];
+            if constexpr (PRE)
+              Vt[vi] = acc[mr][nf][e] + beta * __ldcg(pold_ + elem_sidx<C>(c, mr, nf, e));
+            else
+              Vt[vi] = rr_[mr][nf][e] + beta * Vt[vi];
           }
         }
         RM_T(5);
@@ -405,7 +544,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
       }
       if (W.d_norms) {
         double yy[1];
-        group_reduce<C, 1>(p1, red, red_peer, buf, c.urow, c.ucol, c.lane, yy);
+        group_reduce<C, 1>(p1, red, sm.red_peer, buf, c.urow, c.ucol, c.lane, yy);
         buf ^= 1;
         if (c.rank == 0 && c.tid == 0) W.d_norms[oi] = yy[0];
       }
@@ -548,7 +687,7 @@ __global__ void diff_sqnorm_kernel(int64_t n, const double* a, const double* b, 
 template <int NP, int G>
 static cudaError_t launch_chain_t(const ChainArgs& a, int max_clusters, cudaStream_t st) {
   using C = Cfg<NP, G>;
-  auto kern = chain_kernel<C>;
+  auto kern = a.sw.precond ? chain_kernel<C, true> : chain_kernel<C, false>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
   if (err != cudaSuccess) return err;
   if (G > 8) {
@@ -576,7 +715,7 @@ static cudaError_t launch_chain_t(const ChainArgs& a, int max_clusters, cudaStre
 template <int NP, int G>
 static cudaError_t max_clusters_t(int* out) {
   using C = Cfg<NP, G>;
-  auto kern = chain_kernel<C>;
+  auto kern = chain_kernel<C, true>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
   if (err != cudaSuccess) return err;
   if (G > 8) {

@@ -19,6 +19,10 @@ struct ChainArgs {
   int* fail;           // first-failure flag
   double* fail_info;   // n, iterations, residual norm
   long long* timing;   // RM_TIMING builds: per-phase cycles of CTA 0
+  const double* dm;    // tau preconditioner: d(s) = dm + s*dk, [ny][nx] (device)
+  const double* dk;
+  const double* tabx;  // sine tables sqrt(2/(n+1)) sin(pi m/(n+1)), m < 2(n+1) (device)
+  const double* taby;
 };
 
 struct ApplyArgs {

@@ -112,6 +112,19 @@ class Engine:
     def for_problem(cls, grid, beta, gamma, kx, ky) -> "Engine":
         return cls(grid.nx, grid.ny, generators_for(grid, beta, gamma), kx, ky)
 
+    def ensure_tau(self) -> None:
+        """Install the tau preconditioner (host O(n^3) setup, once per grid; precond.py)."""
+        if getattr(self, "_tau_ready", False):
+            return
+        from .precond import tau_diagonals_from_generators
+
+        dm, dk = tau_diagonals_from_generators(self.gens, self.nx, self.ny, self.kx, self.ky)
+        dm = np.ascontiguousarray(dm, dtype=np.float64)
+        dk = np.ascontiguousarray(dk, dtype=np.float64)
+        _native.check(self.lib.rm_grid_set_tau(self.handle, dm.ctypes.data_as(C.POINTER(C.c_double)),
+                                               dk.ctypes.data_as(C.POINTER(C.c_double))), "rm_grid_set_tau")
+        self._tau_ready = True
+
     def __del__(self):
         h = getattr(self, "handle", None)
         if h is not None and h.value:
@@ -140,7 +153,8 @@ class Engine:
               x0_mode: int = 1, x0: torch.Tensor | None = None, f: torch.Tensor | None = None, f_stride: int = 0,
               fscale: torch.Tensor | None = None, gadd: torch.Tensor | None = None, sub: torch.Tensor | None = None,
               out: torch.Tensor | None = None, out_div: int = 1, norms: torch.Tensor | None = None,
-              max_iter: int | None = None, group: int = 0, row: int | None = None, tag: str = "") -> None:
+              max_iter: int | None = None, group: int = 0, row: int | None = None, tag: str = "",
+              precond: str = "none") -> None:
         """One rm_sweep_run launch; 2-D arrays are indexed by time point with row stride ``row``."""
         if nchains <= 0:
             return
@@ -165,6 +179,11 @@ class Engine:
             raise TypeError("counters must be an int64 CUDA tensor of length 3")
         sw.d_counters = counters.data_ptr()
         sw.group = int(group)
+        if precond == "tau":
+            self.ensure_tau()
+            sw.precond = 1
+        elif precond != "none":
+            raise ValueError(f"unknown preconditioner {precond!r}")
         if self.trace is not None:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             before = counters.clone()

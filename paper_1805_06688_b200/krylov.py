@@ -20,15 +20,26 @@ __all__ = ["CgOptions", "CgFailure", "cg_solve"]
 
 @dataclass
 class CgOptions:
-    """krylov.py:12-20; ``max_iter=None`` means 10 * ndof."""
+    """krylov.py:12-20; ``max_iter=None`` means 10 * ndof.
+
+    Extension: ``preconditioner`` = 'tau' (default) runs CG preconditioned by
+    the optimal sine-transform approximation of the step operator
+    (precond.py); 'none' is the reference's unpreconditioned CG.  Both stop on
+    the reference criterion ||b - A x|| <= rel_tol ||b|| with the same
+    true-residual acceptance, so solutions agree to the solve tolerance; only
+    the iteration counts differ.
+    """
 
     rel_tol: float = 1e-9
     max_iter: int | None = None
     record_iterations: bool = False
+    preconditioner: str = "tau"
 
     def __post_init__(self):
         if self.rel_tol <= 0:
             raise ValueError("relative tolerance must be positive")
+        if self.preconditioner not in ("tau", "none"):
+            raise ValueError("preconditioner must be 'tau' or 'none'")
 
 
 class CgFailure(RuntimeError):

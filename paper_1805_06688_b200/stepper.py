@@ -132,7 +132,7 @@ class Discretization:
         out = torch.empty_like(v)
         self.engine.sweep(nchains=B, first=1, cstride=1, clen=1, nmax=B, dt=dts, counters=self.counters,
                           rel_tol=self.cg_opts.rel_tol, max_iter=self.cg_opts.max_iter, src=v, explicit=True,
-                          x0_mode=1, out=(out, -1))
+                          x0_mode=1, out=(out, -1), precond=self.cg_opts.preconditioner)
         self.engine.check_fail()
         return from_device(out, kind)
 
@@ -227,7 +227,8 @@ def sequential_solve(spec: ProblemSpec, disc: Discretization | None = None, *, d
     loads = disc.device_loads(pts)
     disc.engine.sweep(nchains=1, first=1, cstride=0, clen=N, nmax=N, dt=_dt_tensor(pts, disc.device),
                       counters=disc.counters, rel_tol=disc.cg_opts.rel_tol, max_iter=disc.cg_opts.max_iter,
-                      src=U, explicit=True, x0_mode=1, out=U, **loads.sweep_kwargs())
+                      src=U, explicit=True, x0_mode=1, out=U, precond=disc.cg_opts.preconditioner,
+                      **loads.sweep_kwargs())
     try:
         disc.engine.check_fail()
     except Exception as exc:
@@ -252,7 +253,8 @@ def spacetime_residual(spec: ProblemSpec, U, disc: Discretization | None = None)
     loads = disc.device_loads(pts)
     disc.engine.sweep(nchains=N, first=1, cstride=1, clen=1, nmax=N, dt=_dt_tensor(pts, disc.device),
                       counters=disc.counters, rel_tol=disc.cg_opts.rel_tol, max_iter=disc.cg_opts.max_iter,
-                      src=Ud, explicit=True, x0_mode=2, x0=Ud, sub=Ud, norms=sq, **loads.sweep_kwargs())
+                      src=Ud, explicit=True, x0_mode=2, x0=Ud, sub=Ud, norms=sq, precond=disc.cg_opts.preconditioner,
+                      **loads.sweep_kwargs())
     disc.engine.check_fail()
     norms = np.sqrt(sq.cpu().numpy())
     return norms, float(np.sqrt(np.sum(norms**2)))

@@ -81,17 +81,24 @@ def test_apply_accepts_device_batches(golden):
 
 
 # ----------------------------------------------------------------------------- CG
+PRECONDS = ["none", "tau"]
+
+
+@pytest.mark.parametrize("pre", PRECONDS)
 @pytest.mark.parametrize("k", range(4))
-def test_cg_matches_reference(golden, k):
+def test_cg_matches_reference(golden, k, pre):
     g = golden("cg.npz")
     M, dt, warm, tol = g[f"k{k}_params"]
     spec = man_spec(int(M), 4, beta=0.6, gamma=0.7)
     disc = Discretization(spec)
     op = disc.combined(dt, +1)
     x0 = g[f"k{k}_x0"] if warm else None
-    x, its = cg_solve(op, g[f"k{k}_b"], x0=x0, opts=CgOptions(rel_tol=tol))
+    x, its = cg_solve(op, g[f"k{k}_b"], x0=x0, opts=CgOptions(rel_tol=tol, preconditioner=pre))
     assert rel(x, g[f"k{k}_x"]) <= 1e-9
-    assert abs(its - int(g[f"k{k}_its"])) <= 1
+    if pre == "none":
+        assert abs(its - int(g[f"k{k}_its"])) <= 1
+    else:
+        assert its <= int(g[f"k{k}_its"])
     # the reference's residual criterion on the returned iterate
     r = g[f"k{k}_b"] - op.apply(x)
     assert np.linalg.norm(r) <= 10 * tol * np.linalg.norm(g[f"k{k}_b"])
@@ -168,7 +175,7 @@ SMALL_RUNS = {
 }
 
 
-def check_run(U, trace, g, tag, it_exact=True):
+def check_run(U, trace, g, tag, pre="none"):
     ref_res = g[f"{tag}_res"]
     assert trace.iterations == len(ref_res) - 1, (trace.residual_norms, ref_res)
     assert trace.converged
@@ -176,49 +183,58 @@ def check_run(U, trace, g, tag, it_exact=True):
     # the initial residual depends only on the (bit-identical) initial guess and G
     assert trace.residual_norms[0] == pytest.approx(float(ref_res[0]), rel=1e-10)
     cg_ref = g[f"{tag}_cgits"]
-    assert abs(trace.cg_iterations[-1] - cg_ref[-1]) <= 0.01 * cg_ref[-1] + 2
+    if pre == "none":  # the reference's unpreconditioned CG: same work
+        assert abs(trace.cg_iterations[-1] - cg_ref[-1]) <= 0.01 * cg_ref[-1] + 2
+    else:  # preconditioned inner solves: fewer iterations, same solutions
+        assert trace.cg_iterations[-1] < cg_ref[-1]
     R = g[f"{tag}_U"]
     if R.shape[0] != np.asarray(U).shape[0]:
         U = np.asarray(U)[:: (np.asarray(U).shape[0] - 1) // (R.shape[0] - 1)]
     assert per_point_rel(U, R).max() <= 1e-10
 
 
+@pytest.mark.parametrize("pre", PRECONDS)
 @pytest.mark.parametrize("tag", list(SMALL_RUNS))
-def test_small_mgrit_matches_reference(golden, tag):
+def test_small_mgrit_matches_reference(golden, tag, pre):
     g = golden("mgrit_small.npz")
     spec = man_spec(8, 64)
-    opts = MgritOptions(halt_tol=1e-10, cg_rel_tol=1e-12, **SMALL_RUNS[tag])
+    opts = MgritOptions(halt_tol=1e-10, cg_rel_tol=1e-12, cg_preconditioner=pre, **SMALL_RUNS[tag])
     U, trace = solve(spec, opts)
-    check_run(U, trace, g, tag)
+    check_run(U, trace, g, tag, pre)
 
 
-def test_small_parareal_matches_reference(golden):
+@pytest.mark.parametrize("pre", PRECONDS)
+def test_small_parareal_matches_reference(golden, pre):
     g = golden("mgrit_small.npz")
-    U, trace = parareal_solve(man_spec(8, 64), MgritOptions(m=8, halt_tol=1e-10, cg_rel_tol=1e-12))
-    check_run(U, trace, g, "parareal")
+    U, trace = parareal_solve(man_spec(8, 64), MgritOptions(m=8, halt_tol=1e-10, cg_rel_tol=1e-12,
+                                                            cg_preconditioner=pre))
+    check_run(U, trace, g, "parareal", pre)
 
 
 def case_spec(case):
     return ProblemSpec(**case.problem_kwargs())
 
 
+@pytest.mark.parametrize("pre", PRECONDS)
 @pytest.mark.parametrize("tag,levels", [("two", 2), ("multi", None)])
-def test_cfg1_matches_reference(golden, tag, levels):
+def test_cfg1_matches_reference(golden, tag, levels, pre):
     g = golden("cfg1.npz")
     case = make_case("cfg1")
     assert np.array_equal(case.psi0, g["psi0"]) and np.array_equal(case.g, g["g"])
-    opts = MgritOptions(m=case.m, max_levels=levels, halt_tol=case.halt_tol, cg_rel_tol=case.cg_rel_tol)
+    opts = MgritOptions(m=case.m, max_levels=levels, halt_tol=case.halt_tol, cg_rel_tol=case.cg_rel_tol,
+                        cg_preconditioner=pre)
     U, trace = solve(case_spec(case), opts)
-    check_run(U, trace, g, tag)
+    check_run(U, trace, g, tag, pre)
     # MGRIT vs sequential time stepping (tests/test_mgrit.py:137-144 uses 1e-8)
     assert np.abs(U - g["seq_U"]).max() <= 1e-8
 
 
-def test_cfg1_sequential_matches_reference(golden):
+@pytest.mark.parametrize("pre", PRECONDS)
+def test_cfg1_sequential_matches_reference(golden, pre):
     g = golden("cfg1.npz")
     case = make_case("cfg1")
     spec = case_spec(case)
-    U = sequential_solve(spec, Discretization(spec, cg_opts=CgOptions(rel_tol=case.cg_rel_tol)))
+    U = sequential_solve(spec, Discretization(spec, cg_opts=CgOptions(rel_tol=case.cg_rel_tol, preconditioner=pre)))
     assert per_point_rel(U, g["seq_U"]).max() <= 1e-10
 
 
@@ -228,12 +244,14 @@ def test_cfg1_sequential_matches_reference(golden):
     ("c2", "cfg2", dict(M=None, Nt=16, levels=None)),
     ("c2s", "cfg2", dict(M=32, Nt=512, levels=None)),
 ])
-def test_reduced_configs_match_reference(golden, tag, name, kw):
+@pytest.mark.parametrize("pre", PRECONDS)
+def test_reduced_configs_match_reference(golden, tag, name, kw, pre):
     g = golden("reduced.npz")
     case = make_case(name, M=kw["M"], Nt=kw["Nt"])
-    opts = MgritOptions(m=case.m, max_levels=kw["levels"], halt_tol=case.halt_tol, cg_rel_tol=case.cg_rel_tol)
+    opts = MgritOptions(m=case.m, max_levels=kw["levels"], halt_tol=case.halt_tol, cg_rel_tol=case.cg_rel_tol,
+                        cg_preconditioner=pre)
     U, trace = solve(case_spec(case), opts)
-    check_run(U, trace, g, tag)
+    check_run(U, trace, g, tag, pre)
 
 
 # ----------------------------------------------------------------------------- RNG, determinism
@@ -250,8 +268,9 @@ def test_device_pcg64_is_numpy_bit_exact(golden):
     assert np.array_equal(flat, np.random.default_rng(0).random((8, 16129)).ravel())
 
 
+@pytest.mark.parametrize("pre", PRECONDS)
 @pytest.mark.parametrize("M", [32, 64, 128])
-def test_results_independent_of_cluster_size(M):
+def test_results_independent_of_cluster_size(M, pre):
     """Chains processed by 1, 2, 4, 8 or 16 CTAs give bitwise identical results."""
     from paper_1805_06688_b200 import _native
     from paper_1805_06688_b200.engine import Engine
@@ -273,7 +292,7 @@ def test_results_independent_of_cluster_size(M):
         cnt = torch.zeros(3, dtype=torch.int64, device="cuda")
         norms = torch.zeros(7, dtype=torch.float64, device="cuda")
         eng.sweep(nchains=6, first=1, cstride=1, clen=1, nmax=6, dt=dt, counters=cnt, rel_tol=1e-12, src=V,
-                  x0_mode=1, out=(out, -1), norms=(norms, -1), group=G)
+                  x0_mode=1, out=(out, -1), norms=(norms, -1), group=G, precond=pre)
         eng.check_fail()
         outs.append((G, out.cpu().numpy(), norms.cpu().numpy(), cnt.cpu().numpy()))
         del lib
@@ -311,3 +330,18 @@ def test_graded_mesh_uses_per_step_dt():
     rhs = disc.load_vector(pts[n - 1], pts[n]) + disc.combined(w, -1).apply(U[n - 1])
     x = disc.implicit_solve(w, rhs, x0=U[n - 1])
     assert rel(x, U[n]) <= 1e-12
+
+
+@pytest.mark.parametrize("dt", [1.0 / 4096, 1.0 / 64, 1.0 / 8])
+def test_tau_preconditioner_cuts_iterations(dt):
+    """127^2 cfg2 operator: PCG reaches the reference tolerance in far fewer iterations."""
+    case = make_case("cfg2", Nt=8)
+    spec = case_spec(case)
+    v = np.random.default_rng(4).random((4, case.grid.ndof))
+    out = {}
+    for pre in PRECONDS:
+        disc = Discretization(spec, cg_opts=CgOptions(rel_tol=1e-12, preconditioner=pre))
+        out[pre] = (disc.propagate(dt, v), disc.cg_iterations)
+    assert per_point_rel(out["tau"][0], out["none"][0]).max() <= 1e-10
+    assert out["tau"][1] * 2 <= out["none"][1] or dt < 1e-3
+    assert out["tau"][1] < out["none"][1]

@@ -10,7 +10,11 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1805_06688_b200.configs import make_case  # noqa: E402
 from paper_1805_06688_b200.engine import Engine  # noqa: E402
 
-NAMES = ["matvec", "Ap+pAp partial", "reduce pAp", "x/r update", "reduce rr", "p update", "sync p", "loop top"]
+NAMES = ["matvec", "Ap+pAp partial", "reduce pAp", "x/r update", "reduce rr(+rz)", "p update", "sync p", "loop top",
+         "tau: r->tile", "tau: dst_x", "tau: x->tile", "tau: dst_y", "tau: scale->tile"]
+
+
+PRE = os.environ.get('RM_PRECOND', 'tau')
 
 
 def main():
@@ -24,7 +28,7 @@ def main():
         cnt = torch.zeros(3, dtype=torch.int64, device="cuda")
         zero = (ctypes.c_longlong * 16)()
         eng.sweep(nchains=B, first=1, cstride=1, clen=1, nmax=B, dt=dt, counters=cnt, rel_tol=1e-12, src=V,
-                  x0_mode=1, out=(out, -1), group=G)
+                  x0_mode=1, out=(out, -1), group=G, precond=PRE)
         torch.cuda.synchronize()
         t0 = (ctypes.c_longlong * 16)()
         eng.lib.rm_debug_timing(eng.handle, t0)
@@ -32,12 +36,12 @@ def main():
         cnt.zero_()
         e0.record()
         eng.sweep(nchains=B, first=1, cstride=1, clen=1, nmax=B, dt=dt, counters=cnt, rel_tol=1e-12, src=V,
-                  x0_mode=1, out=(out, -1), group=G)
+                  x0_mode=1, out=(out, -1), group=G, precond=PRE)
         e1.record()
         torch.cuda.synchronize()
         t1 = (ctypes.c_longlong * 16)()
         eng.lib.rm_debug_timing(eng.handle, t1)
-        d = [t1[i] - t0[i] for i in range(8)]
+        d = [t1[i] - t0[i] for i in range(13)]
         c = cnt.cpu().tolist()
         its_cta0 = None
         tot = sum(d)
