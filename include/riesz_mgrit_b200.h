@@ -105,7 +105,8 @@ RM_API int rm_apply_batched(const rm_grid* grid, int which, int batch, const dou
  * spacetime_residual (:187-205), each as one launch.
  * d_counters[0] += number of spatial solves, d_counters[1] += CG iterations
  * (Discretization.spatial_solves / cg_iterations, stepper.py:95-96,114,121),
- * d_counters[2] += operator applies performed (for FLOP accounting).
+ * d_counters[2] += operator applies performed, d_counters[3] += preconditioner applications
+ * (FLOP accounting; the array must hold 4 counters).
  * A CG failure is recorded in the grid's failure slot (rm_fail_info).
  */
 typedef struct rm_sweep {
@@ -134,6 +135,11 @@ typedef struct rm_sweep {
   int group;   /* CTAs per chain (cluster size); 0 = library choice */
   int precond; /* 0: plain CG (the reference algorithm); 1: tau-preconditioned CG (needs
                   rm_grid_set_tau); both stop on ||b - A x|| <= rel_tol ||b|| */
+  /* optional second starting guess x0' = guess_n - G_n (G_n only when d_gadd): the solve starts
+     from whichever of x0, x0' has the smaller initial residual (e.g. the iterate value this step
+     is about to overwrite).  NULL: off. */
+  const double* d_guess;
+  int64_t guess_stride;
 } rm_sweep;
 
 RM_API int rm_sweep_run(rm_grid* grid, const rm_sweep* sweep, void* stream);

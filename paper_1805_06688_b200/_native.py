@@ -41,6 +41,8 @@ class Sweep(C.Structure):
         ("d_counters", C.c_void_p),
         ("group", C.c_int),
         ("precond", C.c_int),
+        ("d_guess", C.c_void_p),
+        ("guess_stride", C.c_int64),
     ]
 
 

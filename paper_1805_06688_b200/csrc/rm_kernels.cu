@@ -73,6 +73,17 @@ __device__ __forceinline__ void load_vec(double* Vt, const double* __restrict__ 
   }
 }
 
+// Vt <- guess - G (G may be null)
+template <class C>
+__device__ __forceinline__ void load_guess(double* Vt, const double* __restrict__ guess, const double* __restrict__ G,
+                                           int nx, int ny, const Ctx<C>& c) {
+  for (int j = c.warp; j < ny; j += C::WARPS) {
+    const int64_t o = (int64_t)j * nx;
+    double* dst = Vt + vt_idx<C>(j, 0);
+    for (int i = c.lane; i < nx; i += 32) dst[i] = G ? __ldcg(guess + o + i) - __ldcg(G + o + i) : __ldcg(guess + o + i);
+  }
+}
+
 template <class C>
 __device__ __forceinline__ void zero_part(double (&p)[C::WR][C::WC]) {
 #pragma unroll
@@ -270,6 +281,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
         matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true);
       }
       int64_t nmv = need_in ? 1 : 0;
+      int64_t npc = 0;  // preconditioner applications
       double part[2][C::WR][C::WC];
       zero_part<C>(part[0]);
       zero_part<C>(part[1]);
@@ -327,6 +339,36 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
       buf ^= 1;
       const double bnorm = sqrt(tot[0]);
       const double target = bnorm > 0.0 ? W.rel_tol * bnorm : W.rel_tol;
+      if (W.d_guess && sqrt(tot[1]) > target) {
+        // second candidate start x0' = guess_n [- G_n] (the value this solve is about to replace);
+        // keep whichever initial residual is smaller (deterministic: both norms are group-reduced)
+        const double* Gr = W.d_gadd ? W.d_gadd + (int64_t)n * W.gadd_stride : nullptr;
+        load_guess<C>(Vt, W.d_guess + (int64_t)n * W.guess_stride, Gr, nx, ny, c);
+        __syncthreads();
+        matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true);
+        ++nmv;
+        double pg[1][C::WR][C::WC];
+        zero_part<C>(pg[0]);
+        RM_FOR_ELEM {
+          const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
+          double r = 0.0;
+          if (j < ny && i < nx)
+            r = sb_[elem_sidx<C>(c, mr, nf, e)] - (mass_stencil<C>(Vt, j, i, cm) + s * acc[mr][nf][e]);
+          acc[mr][nf][e] = r;
+          pg[0][mr][nf >> 1] += r * r;
+        }
+        double rg[1];
+        group_reduce<C, 1>(pg, red, sm.red_peer, buf, c.urow, c.ucol, c.lane, rg);
+        buf ^= 1;
+        if (rg[0] < tot[1]) {
+          tot[1] = rg[0];
+          RM_FOR_ELEM {
+            const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
+            xs[elem_xidx<C>(c, mr, nf, e)] = (j < ny && i < nx) ? Vt[vt_idx<C>(j, i)] : 0.0;
+            rr_[mr][nf][e] = acc[mr][nf][e];
+          }
+        }
+      }
       double res = sqrt(tot[1]);
       double rr = tot[1];  // r.r (CG) or r.z (PCG)
       int64_t its = 0;
@@ -337,6 +379,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
         if constexpr (PRE) {
           // z = P^-1 r, p = z, rz = r.z
           apply_tau<C>(c, sm, bc, rr_, acc, dinv, nx, ny, Lx, Ly, P.timing);
+          ++npc;
           double p1[1][C::WR][C::WC];
           zero_part<C>(p1[0]);
           RM_FOR_ELEM { p1[0][mr][nf >> 1] += rr_[mr][nf][e] * acc[mr][nf][e]; }
@@ -412,6 +455,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
         if constexpr (PRE) {
           // z = P^-1 r; reduce r.r (convergence test) and r.z together
           apply_tau<C>(c, sm, bc, rr_, acc, dinv, nx, ny, Lx, Ly, P.timing);
+          ++npc;
           RM_T0();
           RM_FOR_ELEM { part2[1][mr][nf >> 1] += rr_[mr][nf][e] * acc[mr][nf][e]; }
           group_reduce<C, 2>(part2, red, sm.red_peer, buf, c.urow, c.ucol, c.lane, red2);
@@ -472,6 +516,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           }
           if constexpr (PRE) {
             apply_tau<C>(c, sm, bc, rr_, acc, dinv, nx, ny, Lx, Ly, P.timing);
+            ++npc;
             zero_part<C>(p1[0]);
             RM_FOR_ELEM { p1[0][mr][nf >> 1] += rr_[mr][nf][e] * acc[mr][nf][e]; }
             double rz[1];
@@ -510,6 +555,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
         atomicAdd(W.d_counters, 1ull);
         atomicAdd(W.d_counters + 1, (unsigned long long)its);
         atomicAdd(W.d_counters + 2, (unsigned long long)nmv);
+        atomicAdd(W.d_counters + 3, (unsigned long long)npc);
       }
       if (fail) {
         if (c.rank == 0 && c.tid == 0 && atomicCAS(P.fail, 0, fail) == 0) {

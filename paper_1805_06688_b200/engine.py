@@ -154,7 +154,7 @@ class Engine:
               fscale: torch.Tensor | None = None, gadd: torch.Tensor | None = None, sub: torch.Tensor | None = None,
               out: torch.Tensor | None = None, out_div: int = 1, norms: torch.Tensor | None = None,
               max_iter: int | None = None, group: int = 0, row: int | None = None, tag: str = "",
-              precond: str = "none") -> None:
+              precond: str = "none", guess=None) -> None:
         """One rm_sweep_run launch; 2-D arrays are indexed by time point with row stride ``row``."""
         if nchains <= 0:
             return
@@ -173,10 +173,11 @@ class Engine:
         sw.d_sub, sw.sub_stride = _ptr(sub, row), row
         sw.d_out, sw.out_stride = _ptr(out, row), row
         sw.d_norms = _ptr(norms, 1)
+        sw.d_guess, sw.guess_stride = _ptr(guess, row), row
         sw.rel_tol = float(rel_tol)
         sw.max_iter = -1 if max_iter is None else int(max_iter)
-        if counters.dtype != torch.int64 or not counters.is_cuda or counters.numel() < 3:
-            raise TypeError("counters must be an int64 CUDA tensor of length 3")
+        if counters.dtype != torch.int64 or not counters.is_cuda or counters.numel() < 4:
+            raise TypeError("counters must be an int64 CUDA tensor of length 4")
         sw.d_counters = counters.data_ptr()
         sw.group = int(group)
         if precond == "tau":
@@ -220,14 +221,14 @@ class Engine:
                       "rm_diff_sqnorm")
         self.launches += 1
 
-    def pcg64_fill(self, seed: int, out: torch.Tensor) -> None:
-        """out[:] = np.random.default_rng(seed).random(out.shape), generated on the device."""
+    def pcg64_fill(self, seed: int, out: torch.Tensor, start: int = 0) -> None:
+        """out[:] = draws start.. of np.random.default_rng(seed).random(), generated on the device."""
         st = np.random.default_rng(seed).bit_generator.state["state"]
         s, inc = int(st["state"]), int(st["inc"])
         mask = (1 << 64) - 1
         rows, row = out.shape
-        _native.check(self.lib.rm_pcg64_uniform(s >> 64, s & mask, inc >> 64, inc & mask, 0, rows * row, row,
-                                                _ptr(out), out.stride(0), _stream()), "rm_pcg64_uniform")
+        _native.check(self.lib.rm_pcg64_uniform(s >> 64, s & mask, inc >> 64, inc & mask, int(start), rows * row,
+                                                row, _ptr(out), out.stride(0), _stream()), "rm_pcg64_uniform")
         self.launches += 1
 
 

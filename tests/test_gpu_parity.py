@@ -289,7 +289,7 @@ def test_results_independent_of_cluster_size(M, pre):
         if not _supported(np_, G):
             continue
         out = torch.zeros_like(V)
-        cnt = torch.zeros(3, dtype=torch.int64, device="cuda")
+        cnt = torch.zeros(4, dtype=torch.int64, device="cuda")
         norms = torch.zeros(7, dtype=torch.float64, device="cuda")
         eng.sweep(nchains=6, first=1, cstride=1, clen=1, nmax=6, dt=dt, counters=cnt, rel_tol=1e-12, src=V,
                   x0_mode=1, out=(out, -1), norms=(norms, -1), group=G, precond=pre)

@@ -24,6 +24,10 @@ def fmv(nx, ny):
     return 2 * nx * nx * (3 * ny - 2) + 2 * ny * ny * (3 * nx - 2) + 13 * nx * ny
 
 
+def fpc(nx, ny):
+    return 4 * nx * ny * (nx + ny) + nx * ny
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="cfg2")
@@ -33,13 +37,16 @@ def main():
     ap.add_argument("--repeat", type=int, default=2)
     ap.add_argument("--json", default=None)
     ap.add_argument("--counts-json", default=None)
+    ap.add_argument("--precond", default="tau")
     a = ap.parse_args()
     case = make_case(a.config, M=a.M, Nt=a.nt)
     lv = case.max_levels if a.levels == "default" else (None if a.levels == "none" else int(a.levels))
     spec = ProblemSpec(**case.problem_kwargs())
-    opts = MgritOptions(m=case.m, max_levels=lv, halt_tol=case.halt_tol, cg_rel_tol=case.cg_rel_tol)
+    opts = MgritOptions(m=case.m, max_levels=lv, halt_tol=case.halt_tol, cg_rel_tol=case.cg_rel_tol,
+                        cg_preconditioner=a.precond)
     eng = Engine.for_problem(case.grid, case.beta, case.gamma, case.kx, case.ky)
     F = fmv(case.grid.nx, case.grid.ny)
+    FP = fpc(case.grid.nx, case.grid.ny)
     for rep in range(a.repeat):
         eng.start_trace()
         torch.cuda.synchronize()
@@ -51,23 +58,27 @@ def main():
         agg = collections.OrderedDict()
         tot_ms = 0.0
         tot_mv = 0
+        tot_fl = 0.0
         for tag, e0, e1, before, after, nch in trace:
             ms = e0.elapsed_time(e1)
             d = (after - before).cpu().tolist()
-            s = agg.setdefault(tag, dict(launches=0, ms=0.0, solves=0, cg=0, mv=0, chains=nch))
+            s = agg.setdefault(tag, dict(launches=0, ms=0.0, solves=0, cg=0, mv=0, pc=0, chains=nch))
             s["launches"] += 1
             s["ms"] += ms
             s["solves"] += d[0]
             s["cg"] += d[1]
             s["mv"] += d[2]
+            s["pc"] += d[3]
             tot_ms += ms
             tot_mv += d[2]
+            tot_fl += d[2] * F + d[3] * FP
         print(f"rep {rep}: {case.name} ndof={case.grid.ndof} Nt={case.tmesh.n_intervals} iters={tr.iterations} "
-              f"TTS={tts:.3f}s kernel_ms={tot_ms:.1f} matvecs={tot_mv} achieved={tot_mv * F / tot_ms / 1e9:.2f} TF/s")
+              f"TTS={tts:.3f}s kernel_ms={tot_ms:.1f} matvecs={tot_mv} achieved={tot_fl / tot_ms / 1e9:.2f} TF/s")
         for tag, s in agg.items():
             print(f"  {tag:12s} launches={s['launches']:4d} chains={s['chains']:5d} ms={s['ms']:9.2f} "
                   f"solves={s['solves']:7d} cg/solve={s['cg'] / max(s['solves'], 1):7.1f} "
-                  f"TF/s={s['mv'] * F / max(s['ms'], 1e-9) / 1e9:6.2f}")
+                  f"pc/solve={s['pc'] / max(s['solves'], 1):5.1f} "
+                  f"TF/s={(s['mv'] * F + s['pc'] * FP) / max(s['ms'], 1e-9) / 1e9:6.2f}")
         print("  residuals:", ["%.3e" % r for r in tr.residual_norms])
     if a.counts_json:
         lv = {}
