@@ -1,0 +1,847 @@
+// Chain kernel for large grids (NP = 256, 512: BASELINE configs 3 and 4).
+//
+// The operand vector no longer fits one CTA's shared memory, so it lives in an
+// L2-resident padded copy in global memory ("PV" layout: rows -1..NP, row stride
+// NP+16 doubles, column c at offset c+8, zero halos) and every matvec streams it
+// through shared memory in 32-wide K chunks (cp.async, double buffered):
+//   x-part:  chunk = rows R0-1..R0+128 of the tile band x 32 columns  (A operand)
+//   y-part:  chunk = 32 rows x columns C0-8..C0+135 of the tile band  (B operand)
+// The Toeplitz operand comes from the generator tables in shared memory as in the
+// small-grid kernel.  One CTA owns one 128x128 output tile (16 warps, each a 16x64
+// strip, 32 accumulators per thread); the G = (NP/128)^2 CTAs of a chain form a
+// cluster.  CG state x, r, b (and dinv, p_old for PCG) lives in a fragment-native
+// global scratch (coalesced, L2 resident); p is the PV copy.  Dot products: per
+// unit (fixed lane order) -> per tile (fixed unit order) -> over tiles (tile order).
+// The CG / PCG control flow is the small-grid kernel's (reference stopping rule,
+// true-residual acceptance, restart on drift, second starting guess).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "riesz_mgrit_b200.h"
+#include "rm_device.cuh"
+#include "rm_kernels.h"
+
+namespace rm {
+
+template <int NP_>
+struct BigCfg {
+  static constexpr int NP = NP_;
+  static constexpr int TPR = NP / 128;  // tiles per row
+  static constexpr int G = TPR * TPR;   // CTAs per chain (cluster size)
+  static constexpr int THREADS = 512;
+  static constexpr int WARPS = 16;
+  static constexpr int NF = 8;             // n-fragments per warp (16 x 64 strip)
+  static constexpr int SP = NP + 16;       // PV row stride (doubles)
+  static constexpr int PV = (NP + 2) * SP; // PV vector size (doubles)
+  static constexpr int GL = 2 * NP + 8;    // generator / sine table length
+  static constexpr int XS = 36;            // x-stage row stride (== 4 mod 16)
+  static constexpr int XROWS = 130;
+  static constexpr int YS = 148;           // y-stage row stride (== 4 mod 16)
+  static constexpr int YCOLS = 144;        // C0-8 .. C0+135
+  static constexpr int STAGE = (XROWS * XS > 32 * YS ? XROWS * XS : 32 * YS);  // doubles per stage
+  static constexpr int TE = 128 * 128;     // elements per tile
+  static constexpr size_t SMEM = sizeof(double) * (6 * GL + 2 * GL + 2 * STAGE + 4 * 64 + 2 * 4 * 16) + 64;
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
+};
+
+struct BigCtx {
+  int tid, lane, warp, gq, tig, rank;
+  int R0, C0;   // tile origin
+  int wr, wc0;  // warp strip: unit row wr (0..7), first unit column wc0 (0 or 4)
+};
+
+// element of (nf, e) in the normal mapping, tile coordinates added
+__device__ __forceinline__ int big_row(const BigCtx& c, int e) { return c.R0 + 16 * c.wr + c.gq + 8 * (e >> 1); }
+__device__ __forceinline__ int big_col(const BigCtx& c, int nf, int e) {
+  return c.C0 + 16 * c.wc0 + 8 * nf + 2 * c.tig + (e & 1);
+}
+// transposed mapping (DST-x stage): m over columns (unit wr), n over rows (units wc0..)
+__device__ __forceinline__ int bigT_row(const BigCtx& c, int nf, int e) {
+  return c.R0 + 16 * c.wc0 + 8 * nf + 2 * c.tig + (e & 1);
+}
+__device__ __forceinline__ int bigT_col(const BigCtx& c, int e) { return c.C0 + 16 * c.wr + c.gq + 8 * (e >> 1); }
+// fragment-native index of (nf, e) inside the CTA's scratch vectors
+__device__ __forceinline__ int big_fidx(const BigCtx& c, int nf, int e) {
+  return ((c.warp * 8 + nf) * 4 + e) * 32 + c.lane;
+}
+
+template <class C>
+__device__ __forceinline__ int pv_idx(int j, int i) {
+  return (j + 1) * C::SP + i + 8;
+}
+
+#define RM_BIG_FOR _Pragma("unroll") for (int nf = 0; nf < 8; ++nf) _Pragma("unroll") for (int e = 0; e < 4; ++e)
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// ---- chunk loaders (all threads) ------------------------------------------------------
+template <class C>
+__device__ __forceinline__ void load_xchunk(double* st, const double* __restrict__ pv, int R0, int k0, int tid) {
+  // rows R0-1 .. R0+128 (130), cols k0 .. k0+31 (16 x 16B per row)
+  for (int t = tid; t < C::XROWS * 16; t += C::THREADS) {
+    const int r = t >> 4, q = t & 15;
+    cp_async16(st + r * C::XS + 2 * q, pv + pv_idx<C>(R0 - 1 + r, k0) + 2 * q);
+  }
+}
+template <class C>
+__device__ __forceinline__ void load_ychunk(double* st, const double* __restrict__ pv, int l0, int C0, int tid) {
+  // rows l0 .. l0+31, cols C0-8 .. C0+135 (72 x 16B per row)
+  for (int t = tid; t < 32 * 72; t += C::THREADS) {
+    const int r = t / 72, q = t % 72;
+    cp_async16(st + r * C::YS + 2 * q, pv + pv_idx<C>(l0 + r, C0 - 8) + 2 * q);
+  }
+}
+
+// acc = X + Y (stiffness, generator tables) of the tile, operand streamed from pv
+template <class C>
+__device__ __forceinline__ void big_matvec(const double* __restrict__ pv, const double* __restrict__ gens,
+                                           double* stage, double (&acc)[8][4], const BigCtx& c, int kx_end,
+                                           int ky_end) {
+#pragma unroll
+  for (int nf = 0; nf < 8; ++nf)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[nf][e] = 0.0;
+  double* st[2] = {stage, stage + C::STAGE};
+  // ---- x-part: K = columns
+  const int nkx = kx_end / 32 + ((kx_end & 31) ? 1 : 0);
+  load_xchunk<C>(st[0], pv, c.R0, 0, c.tid);
+  cp_async_commit();
+  for (int ch = 0; ch < nkx; ++ch) {
+    if (ch + 1 < nkx) load_xchunk<C>(st[(ch + 1) & 1], pv, c.R0, 32 * (ch + 1), c.tid);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* s = st[ch & 1];
+    const int k0 = 32 * ch;
+#pragma unroll 1
+    for (int seg = 0; seg < 3; ++seg) {
+      const int delta = seg == 0 ? 0 : (seg == 1 ? 1 : -1);
+      const double* tab = gens + seg * C::GL + C::NP + c.C0 + 16 * c.wc0 + c.gq - c.tig - k0;
+      const double* ar = s + (16 * c.wr + c.gq + delta + 1) * C::XS + c.tig;
+#pragma unroll 4
+      for (int k = 0; k < 32; k += 4) {
+        const double a0 = ar[k], a1 = ar[k + 8 * C::XS];
+        double b[8];
+#pragma unroll
+        for (int nf = 0; nf < 8; ++nf) b[nf] = tab[8 * nf - k];
+#pragma unroll
+        for (int nf = 0; nf < 8; ++nf) dmma(acc[nf], a0, a1, b[nf]);
+      }
+    }
+    __syncthreads();
+  }
+  // ---- y-part: K = rows
+  const int nky = ky_end / 32 + ((ky_end & 31) ? 1 : 0);
+  load_ychunk<C>(st[0], pv, 0, c.C0, c.tid);
+  cp_async_commit();
+  for (int ch = 0; ch < nky; ++ch) {
+    if (ch + 1 < nky) load_ychunk<C>(st[(ch + 1) & 1], pv, 32 * (ch + 1), c.C0, c.tid);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* s = st[ch & 1];
+    const int l0 = 32 * ch;
+#pragma unroll 1
+    for (int seg = 0; seg < 3; ++seg) {
+      const int delta = seg == 0 ? 0 : (seg == 1 ? 1 : -1);
+      const double* tab = gens + (3 + seg) * C::GL + C::NP + c.R0 + 16 * c.wr + c.gq - c.tig - l0;
+      const double* br = s + c.tig * C::YS + 16 * c.wc0 + c.gq + delta + 8;
+#pragma unroll 4
+      for (int l = 0; l < 32; l += 4) {
+        const double a0 = tab[-l], a1 = tab[8 - l];
+        double b[8];
+#pragma unroll
+        for (int nf = 0; nf < 8; ++nf) b[nf] = br[l * C::YS + 8 * nf];
+#pragma unroll
+        for (int nf = 0; nf < 8; ++nf) dmma(acc[nf], a0, a1, b[nf]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// DST along x in the transposed mapping: out^T[i][j] = sum_k Sx[i][k] V[j][k]
+template <class C>
+__device__ __forceinline__ void big_dst_xT(const double* __restrict__ pv, const double* __restrict__ tab, int L,
+                                           double* stage, double (&acc)[8][4], const BigCtx& c, int kx_end) {
+#pragma unroll
+  for (int nf = 0; nf < 8; ++nf)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[nf][e] = 0.0;
+  double* st[2] = {stage, stage + C::STAGE};
+  const int nkx = kx_end / 32 + ((kx_end & 31) ? 1 : 0);
+  const int xa = c.C0 + 16 * c.wr + c.gq + 1, xb = xa + 8;
+  int ia = (xa * (c.tig + 1)) % L, ib = (xb * (c.tig + 1)) % L;
+  const int sa = (4 * xa) % L, sb = (4 * xb) % L;
+  load_xchunk<C>(st[0], pv, c.R0, 0, c.tid);
+  cp_async_commit();
+  for (int ch = 0; ch < nkx; ++ch) {
+    if (ch + 1 < nkx) load_xchunk<C>(st[(ch + 1) & 1], pv, c.R0, 32 * (ch + 1), c.tid);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* br = st[ch & 1] + (16 * c.wc0 + c.gq + 1) * C::XS + c.tig;
+#pragma unroll 4
+    for (int k = 0; k < 32; k += 4) {
+      const double a0 = tab[ia], a1 = tab[ib];
+      double b[8];
+#pragma unroll
+      for (int nf = 0; nf < 8; ++nf) b[nf] = br[8 * nf * C::XS + k];
+#pragma unroll
+      for (int nf = 0; nf < 8; ++nf) dmma(acc[nf], a0, a1, b[nf]);
+      ia += sa;
+      ia -= ia >= L ? L : 0;
+      ib += sb;
+      ib -= ib >= L ? L : 0;
+    }
+    __syncthreads();
+  }
+}
+
+// DST along y in the normal mapping: out[j][i] = sum_l Sy[j][l] V[l][i]
+template <class C>
+__device__ __forceinline__ void big_dst_y(const double* __restrict__ pv, const double* __restrict__ tab, int L,
+                                          double* stage, double (&acc)[8][4], const BigCtx& c, int ky_end) {
+#pragma unroll
+  for (int nf = 0; nf < 8; ++nf)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[nf][e] = 0.0;
+  double* st[2] = {stage, stage + C::STAGE};
+  const int nky = ky_end / 32 + ((ky_end & 31) ? 1 : 0);
+  const int ja = c.R0 + 16 * c.wr + c.gq + 1, jb = ja + 8;
+  int ia = (ja * (c.tig + 1)) % L, ib = (jb * (c.tig + 1)) % L;
+  const int sa = (4 * ja) % L, sb = (4 * jb) % L;
+  load_ychunk<C>(st[0], pv, 0, c.C0, c.tid);
+  cp_async_commit();
+  for (int ch = 0; ch < nky; ++ch) {
+    if (ch + 1 < nky) load_ychunk<C>(st[(ch + 1) & 1], pv, 32 * (ch + 1), c.C0, c.tid);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* br = st[ch & 1] + c.tig * C::YS + 16 * c.wc0 + c.gq + 8;
+#pragma unroll 4
+    for (int l = 0; l < 32; l += 4) {
+      const double a0 = tab[ia], a1 = tab[ib];
+      double b[8];
+#pragma unroll
+      for (int nf = 0; nf < 8; ++nf) b[nf] = br[l * C::YS + 8 * nf];
+#pragma unroll
+      for (int nf = 0; nf < 8; ++nf) dmma(acc[nf], a0, a1, b[nf]);
+      ia += sa;
+      ia -= ia >= L ? L : 0;
+      ib += sb;
+      ib -= ib >= L ? L : 0;
+    }
+    __syncthreads();
+  }
+}
+
+template <class C>
+__device__ __forceinline__ double big_mass(const double* __restrict__ pv, int j, int i, double cm) {
+  const double* q = pv + pv_idx<C>(j, i);
+  double s = 6.0 * __ldcg(q);
+  s += __ldcg(q - 1);
+  s += __ldcg(q + 1);
+  s += __ldcg(q + C::SP);
+  s += __ldcg(q + C::SP + 1);
+  s += __ldcg(q - C::SP);
+  s += __ldcg(q - C::SP - 1);
+  return cm * s;
+}
+
+// Deterministic group sum of NV values: unit (warp butterfly) -> tile (unit order) -> group (tile order).
+template <class C, int NV>
+__device__ __forceinline__ void big_reduce(double (&part)[NV][4], double* wred, double* tred,
+                                           double* const* tred_peer, int buf, const BigCtx& c, double (&out)[NV]) {
+  // part[v][u]: this thread's partial for its warp strip's unit u (4 units per warp)
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) part[v][u] = warp_allsum(part[v][u]);
+  if (c.lane == 0) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) wred[v * 64 + c.wr * 8 + c.wc0 + u] = part[v][u];
+  }
+  __syncthreads();
+  if (c.warp == 0) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      double x = wred[v * 64 + c.lane] + wred[v * 64 + 32 + c.lane];
+      x = warp_allsum(x);
+      if (c.lane < C::G) tred_peer[c.lane][buf * 4 * 16 + v * 16 + c.rank] = x;
+    }
+  }
+  group_sync<C::G>();
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    double x = c.lane < C::G ? tred[buf * 4 * 16 + v * 16 + c.lane] : 0.0;
+    out[v] = warp_allsum(x);
+  }
+}
+
+template <class C, bool PRE>
+__global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
+  extern __shared__ __align__(16) double smem[];
+  double* gens = smem;
+  double* tabx = gens + 6 * C::GL;
+  double* taby = tabx + C::GL;
+  double* stage = taby + C::GL;
+  double* wred = stage + 2 * C::STAGE;  // 4 values x 64 units
+  double* tred = wred + 4 * 64;         // 2 buffers x 4 values x 16 tiles
+  int* sched = reinterpret_cast<int*>(tred + 2 * 4 * 16);
+
+  BigCtx c;
+  c.tid = threadIdx.x;
+  c.lane = c.tid & 31;
+  c.warp = c.tid >> 5;
+  c.gq = c.lane >> 2;
+  c.tig = c.lane & 3;
+  c.rank = (int)cgx::this_cluster().block_rank();
+  c.R0 = 128 * (c.rank / C::TPR);
+  c.C0 = 128 * (c.rank % C::TPR);
+  c.wr = c.warp >> 1;
+  c.wc0 = (c.warp & 1) * 4;
+
+  double* tred_peer[C::G];
+  int* sched_peer[C::G];
+  {
+    auto cl = cgx::this_cluster();
+#pragma unroll
+    for (int q = 0; q < C::G; ++q) {
+      tred_peer[q] = cl.map_shared_rank(tred, q);
+      sched_peer[q] = cl.map_shared_rank(sched, q);
+    }
+  }
+
+  const rm_sweep& W = P.sw;
+  const int nx = P.nx, ny = P.ny, ndof = nx * ny;
+  const int kx_end = (nx + 3) & ~3, ky_end = (ny + 3) & ~3;
+  const int Lx = 2 * (nx + 1), Ly = 2 * (ny + 1);
+  const double cm = P.cm;
+  const int64_t max_iter = W.max_iter > 0 ? W.max_iter : 10 * (int64_t)ndof;
+  const bool need_in = W.explicit_rhs || W.x0_mode == 1;
+
+  for (int i = c.tid; i < 6 * C::GL; i += C::THREADS) gens[i] = P.gens[i];
+  if constexpr (PRE) {
+    for (int i = c.tid; i < Lx; i += C::THREADS) tabx[i] = P.tabx[i];
+    for (int i = c.tid; i < Ly; i += C::THREADS) taby[i] = P.taby[i];
+  }
+
+  // per-cluster scratch: two PV vectors, then per-CTA fragment-native vectors
+  const int cid = blockIdx.x / C::G;
+  double* base = P.scratch + (size_t)cid * (2 * (size_t)C::PV + 5 * (size_t)C::G * C::TE);
+  double* pv0 = base;           // operand: p, the step input, x for true-residual checks
+  double* pv1 = base + C::PV;   // preconditioner temporary
+  double* fr = base + 2 * C::PV + (size_t)c.rank * 5 * C::TE;
+  double* __restrict__ xs = fr;              // iterate x
+  double* __restrict__ rs = fr + C::TE;      // residual r
+  double* __restrict__ bs = fr + 2 * C::TE;  // right-hand side b
+  double* __restrict__ ds = fr + 3 * C::TE;  // 1 / d(s)
+  double* __restrict__ ps = fr + 4 * C::TE;  // p_old (PCG)
+  // zero the PV halos / padding of this cluster's vectors once (only interior points are ever written)
+  for (size_t i = (size_t)c.rank * C::THREADS + c.tid; i < 2 * (size_t)C::PV; i += (size_t)C::G * C::THREADS)
+    base[i] = 0.0;
+  group_sync<C::G>();
+
+  int buf = 0;
+  double acc[8][4];
+
+  auto put_tile = [&](double* pv, int j, int i, double v) { pv[pv_idx<C>(j, i)] = v; };
+
+  for (;;) {
+    if (c.rank == 0 && c.tid == 0) {
+      const int ch = atomicAdd(P.chain_counter, 1);
+#pragma unroll
+      for (int q = 0; q < C::G; ++q) sched_peer[q][0] = ch;
+    }
+    group_sync<C::G>();
+    const int chain = sched[0];
+    group_sync<C::G>();
+    if (chain >= W.nchains) break;
+    const int n0 = W.first + chain * W.cstride;
+    const int n1 = min(n0 + W.clen - 1, W.nmax);
+    bool in_tile = false;
+    for (int n = n0; n <= n1; ++n) {
+      const double s = 0.5 * W.d_dt[n - 1];
+      const double fs = W.d_f ? (W.d_fscale ? W.d_fscale[n] : 1.0) : 0.0;
+      const double* Fn = W.d_f ? W.d_f + (int64_t)n * W.f_stride : nullptr;
+      int64_t nmv = need_in ? 1 : 0, npc = 0;
+
+      if (need_in) {
+        if (!in_tile) {
+          const double* src = W.d_src + (int64_t)(n - 1) * W.src_stride;
+          RM_BIG_FOR {
+            const int j = big_row(c, e), i = big_col(c, nf, e);
+            if (j < ny && i < nx) put_tile(pv0, j, i, __ldcg(src + j * nx + i));
+          }
+          group_sync<C::G>();
+        }
+        big_matvec<C>(pv0, gens, stage, acc, c, kx_end, ky_end);
+      }
+      double part[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+      RM_BIG_FOR {
+        const int j = big_row(c, e), i = big_col(c, nf, e);
+        const int fi = big_fidx(c, nf, e);
+        double b = 0.0, x = 0.0, r = 0.0;
+        if (j < ny && i < nx) {
+          double mv = 0.0, kv = 0.0;
+          if (need_in) {
+            mv = big_mass<C>(pv0, j, i, cm);
+            kv = acc[nf][e];
+          }
+          if (W.explicit_rhs) b = mv + (-s) * kv;
+          if (Fn) {
+            const double f = fs * __ldcg(Fn + j * nx + i);
+            b = W.explicit_rhs ? f + b : f;
+          }
+          if (W.x0_mode == 1) {
+            x = __ldcg(pv0 + pv_idx<C>(j, i));
+            r = b - (mv + s * kv);
+          } else {
+            r = b;
+          }
+          if constexpr (PRE) ds[fi] = 1.0 / (__ldg(P.dm + j * nx + i) + s * __ldg(P.dk + j * nx + i));
+        }
+        bs[fi] = b;
+        xs[fi] = x;
+        rs[fi] = r;
+        part[0][nf >> 1] += b * b;
+        part[1][nf >> 1] += r * r;
+      }
+      if (W.x0_mode == 2) {
+        group_sync<C::G>();
+        const double* x0 = W.d_x0 + (int64_t)n * W.x0_stride;
+        RM_BIG_FOR {
+          const int j = big_row(c, e), i = big_col(c, nf, e);
+          if (j < ny && i < nx) put_tile(pv0, j, i, __ldcg(x0 + j * nx + i));
+        }
+        group_sync<C::G>();
+        big_matvec<C>(pv0, gens, stage, acc, c, kx_end, ky_end);
+        ++nmv;
+        part[1][0] = part[1][1] = part[1][2] = part[1][3] = 0.0;
+        RM_BIG_FOR {
+          const int j = big_row(c, e), i = big_col(c, nf, e);
+          const int fi = big_fidx(c, nf, e);
+          double x = 0.0, r = 0.0;
+          if (j < ny && i < nx) {
+            x = __ldcg(pv0 + pv_idx<C>(j, i));
+            r = bs[fi] - (big_mass<C>(pv0, j, i, cm) + s * acc[nf][e]);
+          }
+          xs[fi] = x;
+          rs[fi] = r;
+          part[1][nf >> 1] += r * r;
+        }
+      }
+      double tot[2];
+      big_reduce<C, 2>(part, wred, tred, tred_peer, buf, c, tot);
+      buf ^= 1;
+      const double bnorm = sqrt(tot[0]);
+      const double target = bnorm > 0.0 ? W.rel_tol * bnorm : W.rel_tol;
+      if (W.d_guess && sqrt(tot[1]) > target) {
+        const double* gu = W.d_guess + (int64_t)n * W.guess_stride;
+        const double* Gr = W.d_gadd ? W.d_gadd + (int64_t)n * W.gadd_stride : nullptr;
+        RM_BIG_FOR {
+          const int j = big_row(c, e), i = big_col(c, nf, e);
+          if (j < ny && i < nx) {
+            const int gi = j * nx + i;
+            put_tile(pv0, j, i, Gr ? __ldcg(gu + gi) - __ldcg(Gr + gi) : __ldcg(gu + gi));
+          }
+        }
+        group_sync<C::G>();
+        big_matvec<C>(pv0, gens, stage, acc, c, kx_end, ky_end);
+        ++nmv;
+        double pg[1][4] = {{0, 0, 0, 0}};
+        RM_BIG_FOR {
+          const int j = big_row(c, e), i = big_col(c, nf, e);
+          double r = 0.0;
+          if (j < ny && i < nx) r = bs[big_fidx(c, nf, e)] - (big_mass<C>(pv0, j, i, cm) + s * acc[nf][e]);
+          acc[nf][e] = r;
+          pg[0][nf >> 1] += r * r;
+        }
+        double rg[1];
+        big_reduce<C, 1>(pg, wred, tred, tred_peer, buf, c, rg);
+        buf ^= 1;
+        if (rg[0] < tot[1]) {
+          tot[1] = rg[0];
+          RM_BIG_FOR {
+            const int j = big_row(c, e), i = big_col(c, nf, e);
+            const int fi = big_fidx(c, nf, e);
+            xs[fi] = (j < ny && i < nx) ? __ldcg(pv0 + pv_idx<C>(j, i)) : 0.0;
+            rs[fi] = acc[nf][e];
+          }
+        }
+      }
+      double res = sqrt(tot[1]);
+      double rr = tot[1];
+      int64_t its = 0;
+      int fail = 0;
+      bool done = res <= target;
+
+      // z = P^-1 r (PRE) into acc; uses pv1 <- r, pv0 <- T1, pv1 <- T2 * dinv, pv0 <- T3
+      auto apply_tau_big = [&]() {
+        __syncthreads();
+        group_sync<C::G>();  // every CTA done reading pv0 / pv1
+        RM_BIG_FOR {
+          const int j = big_row(c, e), i = big_col(c, nf, e);
+          if (j < ny && i < nx) put_tile(pv1, j, i, __ldcg(rs + big_fidx(c, nf, e)));
+        }
+        group_sync<C::G>();
+#pragma unroll 1
+        for (int pass = 0; pass < 2; ++pass) {
+          big_dst_xT<C>(pv1, tabx, Lx, stage, acc, c, kx_end);
+          RM_BIG_FOR {
+            const int j = bigT_row(c, nf, e), i = bigT_col(c, e);
+            if (j < ny && i < nx) put_tile(pv0, j, i, acc[nf][e]);
+          }
+          group_sync<C::G>();
+          big_dst_y<C>(pv0, taby, Ly, stage, acc, c, ky_end);
+          if (pass == 1) break;
+          RM_BIG_FOR {
+            const int j = big_row(c, e), i = big_col(c, nf, e);
+            if (j < ny && i < nx) put_tile(pv1, j, i, acc[nf][e] * __ldcg(ds + big_fidx(c, nf, e)));
+          }
+          group_sync<C::G>();
+        }
+        ++npc;
+      };
+      auto set_direction_from = [&](bool use_z) {
+        // p = z (PRE) or r into pv0 (after every CTA finished reading pv0)
+        group_sync<C::G>();
+        RM_BIG_FOR {
+          const int j = big_row(c, e), i = big_col(c, nf, e);
+          if (j < ny && i < nx) put_tile(pv0, j, i, use_z ? acc[nf][e] : __ldcg(rs + big_fidx(c, nf, e)));
+        }
+        group_sync<C::G>();
+      };
+
+      if (!done) {
+        if constexpr (PRE) {
+          apply_tau_big();
+          double p1[1][4] = {{0, 0, 0, 0}};
+          RM_BIG_FOR { p1[0][nf >> 1] += __ldcg(rs + big_fidx(c, nf, e)) * acc[nf][e]; }
+          double rz[1];
+          big_reduce<C, 1>(p1, wred, tred, tred_peer, buf, c, rz);
+          buf ^= 1;
+          rr = rz[0];
+          set_direction_from(true);
+        } else {
+          set_direction_from(false);
+        }
+      }
+      for (int64_t k = 1; !done; ++k) {
+        if (k > max_iter) {
+          fail = RM_CG_BUDGET;
+          its = max_iter;
+          break;
+        }
+        big_matvec<C>(pv0, gens, stage, acc, c, kx_end, ky_end);
+        ++nmv;
+        double p1[1][4] = {{0, 0, 0, 0}};
+        RM_BIG_FOR {
+          const int j = big_row(c, e), i = big_col(c, nf, e);
+          double ap = 0.0;
+          if (j < ny && i < nx) {
+            ap = big_mass<C>(pv0, j, i, cm) + s * acc[nf][e];
+            p1[0][nf >> 1] += __ldcg(pv0 + pv_idx<C>(j, i)) * ap;
+          }
+          acc[nf][e] = ap;
+        }
+        double pap[1];
+        big_reduce<C, 1>(p1, wred, tred, tred_peer, buf, c, pap);
+        buf ^= 1;
+        if (!isfinite(pap[0]) || pap[0] <= 0.0) {
+          fail = RM_CG_BREAKDOWN;
+          its = k;
+          break;
+        }
+        const double alpha = rr / pap[0];
+        double part2[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {  // one unit (8 elements) per batch: loads first, then stores
+          double pv[8], xv[8], rv[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int nf = 2 * u + (q >> 2), e = q & 3;
+            const int j = big_row(c, e), i = big_col(c, nf, e);
+            const int fi = big_fidx(c, nf, e);
+            const bool ok = j < ny && i < nx;
+            pv[q] = ok ? __ldcg(pv0 + pv_idx<C>(j, i)) : 0.0;
+            xv[q] = __ldcg(xs + fi);
+            rv[q] = __ldcg(rs + fi);
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int nf = 2 * u + (q >> 2), e = q & 3;
+            const int j = big_row(c, e), i = big_col(c, nf, e);
+            const int fi = big_fidx(c, nf, e);
+            if (j < ny && i < nx) {
+              xs[fi] = xv[q] + alpha * pv[q];
+              const double rn = rv[q] - alpha * acc[nf][e];
+              rs[fi] = rn;
+              part2[0][u] += rn * rn;
+              if constexpr (PRE) ps[fi] = pv[q];
+            }
+          }
+        }
+        double red2[2];
+        if constexpr (PRE) {
+          apply_tau_big();
+          RM_BIG_FOR { part2[1][nf >> 1] += __ldcg(rs + big_fidx(c, nf, e)) * acc[nf][e]; }
+          big_reduce<C, 2>(part2, wred, tred, tred_peer, buf, c, red2);
+        } else {
+          double p0[1][4] = {{part2[0][0], part2[0][1], part2[0][2], part2[0][3]}};
+          double one[1];
+          big_reduce<C, 1>(p0, wred, tred, tred_peer, buf, c, one);
+          red2[0] = red2[1] = one[0];
+        }
+        buf ^= 1;
+        double rr_new = red2[0];
+        res = sqrt(rr_new);
+        if (!isfinite(res)) {
+          fail = RM_CG_NONFINITE;
+          its = k;
+          break;
+        }
+        if (res <= target) {
+          group_sync<C::G>();
+          RM_BIG_FOR {
+            const int j = big_row(c, e), i = big_col(c, nf, e);
+            if (j < ny && i < nx) put_tile(pv0, j, i, xs[big_fidx(c, nf, e)]);
+          }
+          group_sync<C::G>();
+          big_matvec<C>(pv0, gens, stage, acc, c, kx_end, ky_end);
+          ++nmv;
+          double pt[1][4] = {{0, 0, 0, 0}};
+          RM_BIG_FOR {
+            const int j = big_row(c, e), i = big_col(c, nf, e);
+            double rt = 0.0;
+            if (j < ny && i < nx) rt = bs[big_fidx(c, nf, e)] - (big_mass<C>(pv0, j, i, cm) + s * acc[nf][e]);
+            acc[nf][e] = rt;
+            pt[0][nf >> 1] += rt * rt;
+          }
+          double tt[1];
+          big_reduce<C, 1>(pt, wred, tred, tred_peer, buf, c, tt);
+          buf ^= 1;
+          const double true_res = sqrt(tt[0]);
+          if (true_res <= fmax(target, 10.0 * res)) {
+            its = k;
+            done = true;
+            break;
+          }
+          res = true_res;
+          RM_BIG_FOR { rs[big_fidx(c, nf, e)] = acc[nf][e]; }
+          if (res <= target) {
+            its = k;
+            done = true;
+            break;
+          }
+          if constexpr (PRE) {
+            apply_tau_big();
+            double p3[1][4] = {{0, 0, 0, 0}};
+            RM_BIG_FOR { p3[0][nf >> 1] += __ldcg(rs + big_fidx(c, nf, e)) * acc[nf][e]; }
+            double rz[1];
+            big_reduce<C, 1>(p3, wred, tred, tred_peer, buf, c, rz);
+            buf ^= 1;
+            rr = rz[0];
+            set_direction_from(true);
+          } else {
+            rr = tt[0];
+            set_direction_from(false);
+          }
+          continue;
+        }
+        const double beta = red2[1] / rr;
+        rr = red2[1];
+        group_sync<C::G>();  // every CTA done reading pv0 (and the DST stages)
+        RM_BIG_FOR {
+          const int j = big_row(c, e), i = big_col(c, nf, e);
+          if (j < ny && i < nx) {
+            const int fi = big_fidx(c, nf, e);
+            const double pold = PRE ? __ldcg(ps + fi) : __ldcg(pv0 + pv_idx<C>(j, i));
+            const double zi = PRE ? acc[nf][e] : rs[fi];
+            put_tile(pv0, j, i, zi + beta * pold);
+          }
+        }
+        group_sync<C::G>();
+      }
+
+      if (c.rank == 0 && c.tid == 0) {
+        atomicAdd(W.d_counters, 1ull);
+        atomicAdd(W.d_counters + 1, (unsigned long long)its);
+        atomicAdd(W.d_counters + 2, (unsigned long long)nmv);
+        atomicAdd(W.d_counters + 3, (unsigned long long)npc);
+      }
+      if (fail) {
+        if (c.rank == 0 && c.tid == 0 && atomicCAS(P.fail, 0, fail) == 0) {
+          P.fail_info[0] = (double)n;
+          P.fail_info[1] = (double)its;
+          P.fail_info[2] = res;
+        }
+        group_sync<C::G>();
+        break;
+      }
+      // ---------------- MGRIT epilogue ----------------
+      const bool next_in_tile = n < n1 && need_in;
+      const int oi = n / W.out_div;
+      const double* Gn = W.d_gadd ? W.d_gadd + (int64_t)n * W.gadd_stride : nullptr;
+      const double* Sn = W.d_sub ? W.d_sub + (int64_t)n * W.sub_stride : nullptr;
+      double* On = W.d_out ? W.d_out + (int64_t)oi * W.out_stride : nullptr;
+      group_sync<C::G>();  // every CTA done reading pv0 before it is overwritten with y
+      double py[1][4] = {{0, 0, 0, 0}};
+      RM_BIG_FOR {
+        const int j = big_row(c, e), i = big_col(c, nf, e);
+        if (j < ny && i < nx) {
+          const int gi = j * nx + i;
+          double y = xs[big_fidx(c, nf, e)];
+          if (Gn) y = __ldcg(Gn + gi) + y;
+          if (Sn) y = y - __ldcg(Sn + gi);
+          if (On) On[gi] = y;
+          if (next_in_tile) put_tile(pv0, j, i, y);
+          py[0][nf >> 1] += y * y;
+        }
+      }
+      if (W.d_norms) {
+        double yy[1];
+        big_reduce<C, 1>(py, wred, tred, tred_peer, buf, c, yy);
+        buf ^= 1;
+        if (c.rank == 0 && c.tid == 0) W.d_norms[oi] = yy[0];
+      }
+      in_tile = next_in_tile;
+      group_sync<C::G>();
+    }
+  }
+}
+
+// Batched operator apply for large grids (rm_apply_batched; setup and tests, not the hot path):
+// one thread per output element, DFMA over the Toeplitz sums, operand read from global memory.
+__global__ void apply_big_kernel(const ApplyArgs P, int np) {
+  const int nx = P.nx, ny = P.ny;
+  const int b = blockIdx.y;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nx * ny) return;
+  const int j = idx / nx, i = idx % nx;
+  const double* v = P.v + (int64_t)b * P.v_stride;
+  const int GL = 2 * np + 8;
+  const double* g = P.gens + np;
+  auto V = [&](int jj, int ii) { return (jj < 0 || jj >= ny || ii < 0 || ii >= nx) ? 0.0 : __ldg(v + jj * nx + ii); };
+  const bool dox = P.which == 0 || P.which == 2, doy = P.which == 0 || P.which == 3;
+  double acc = 0.0;
+  if (dox)
+    for (int seg = 0; seg < 3; ++seg) {
+      const int d = seg == 0 ? 0 : (seg == 1 ? 1 : -1);
+      for (int k = 0; k < nx; ++k) acc = fma(g[seg * GL + i - k], V(j + d, k), acc);
+    }
+  if (doy)
+    for (int seg = 0; seg < 3; ++seg) {
+      const int d = seg == 0 ? 0 : (seg == 1 ? 1 : -1);
+      for (int l = 0; l < ny; ++l) acc = fma(g[(3 + seg) * GL + j - l], V(l, i + d), acc);
+    }
+  double mass = 6.0 * V(j, i);
+  mass += V(j, i - 1);
+  mass += V(j, i + 1);
+  mass += V(j + 1, i);
+  mass += V(j + 1, i + 1);
+  mass += V(j - 1, i);
+  mass += V(j - 1, i - 1);
+  mass *= P.cm;
+  double y;
+  if (P.which == 1)
+    y = mass;
+  else if (P.which == 0)
+    y = mass + P.sign * 0.5 * P.dt[b] * acc;
+  else
+    y = (P.which == 2 ? 1.0 / P.kx : 1.0 / P.ky) * acc;
+  P.out[(int64_t)b * P.out_stride + idx] = y;
+}
+
+cudaError_t launch_apply_big(int np, const ApplyArgs& a, int batch, cudaStream_t st) {
+  dim3 grid((a.nx * a.ny + 255) / 256, batch);
+  apply_big_kernel<<<grid, 256, 0, st>>>(a, np);
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------------------
+template <int NP>
+static cudaError_t launch_big_t(const ChainArgs& a, int max_clusters, cudaStream_t st) {
+  using C = BigCfg<NP>;
+  auto kern = a.sw.precond ? chain_big_kernel<C, true> : chain_big_kernel<C, false>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  if (err != cudaSuccess) return err;
+  if (C::G > 8) {
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (err != cudaSuccess) return err;
+  }
+  int ncl = max_clusters < a.sw.nchains ? max_clusters : a.sw.nchains;
+  if (ncl < 1) ncl = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ncl * C::G);
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C::G;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+template <int NP>
+static cudaError_t max_clusters_big_t(int* out) {
+  using C = BigCfg<NP>;
+  auto kern = chain_big_kernel<C, true>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  if (err != cudaSuccess) return err;
+  if (C::G > 8) {
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (err != cudaSuccess) return err;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C::G);
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C::G;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaOccupancyMaxActiveClusters(out, kern, &cfg);
+}
+
+bool big_supported(int np) { return np == 256 || np == 512; }
+
+int big_group(int np) { return (np / 128) * (np / 128); }
+
+size_t big_scratch_doubles_per_cluster(int np) {
+  const size_t pv = (size_t)(np + 2) * (np + 16);
+  return 2 * pv + 5 * (size_t)big_group(np) * 128 * 128;
+}
+
+cudaError_t launch_big(int np, const ChainArgs& a, int max_clusters, cudaStream_t st) {
+  if (np == 256) return launch_big_t<256>(a, max_clusters, st);
+  if (np == 512) return launch_big_t<512>(a, max_clusters, st);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t big_max_clusters(int np, int* out) {
+  if (np == 256) return max_clusters_big_t<256>(out);
+  if (np == 512) return max_clusters_big_t<512>(out);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace rm

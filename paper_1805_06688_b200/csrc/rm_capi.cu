@@ -64,7 +64,7 @@ const char* rm_version(void) { return "riesz_mgrit_b200 0.1.0 (sm_100a, FP64 DMM
 
 const char* rm_last_error(void) { return g_err.c_str(); }
 
-int rm_max_order(void) { return 128; }
+int rm_max_order(void) { return 512; }
 
 int rm_grid_create(int nx, int ny, const double* t1x_col, const double* t1x_row, const double* t2x_col,
                    const double* t2x_row, const double* t1y_col, const double* t1y_row, const double* t2y_col,
@@ -110,7 +110,20 @@ int rm_grid_create(int nx, int ny, const double* t1x_col, const double* t1x_row,
   }
   cudaError_t e;
   int maxc = 1;
-  for (int gi = 0; gi < 5; ++gi) {
+  size_t scratch_per_cluster = 3 * (size_t)np * np;
+  if (rm::big_supported(np)) {
+    int n = 0;
+    e = rm::big_max_clusters(np, &n);
+    if (e != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      delete g;
+      return fail(RM_EUNSUP, "rm_grid_create: no resident cluster for the large-grid kernel");
+    }
+    for (int gi = 0; gi < 5; ++gi) g->max_clusters[gi] = kGroups[gi] == rm::big_group(np) ? n : 0;
+    maxc = n;
+    scratch_per_cluster = rm::big_scratch_doubles_per_cluster(np);
+  }
+  for (int gi = 0; gi < 5 && !rm::big_supported(np); ++gi) {
     const int G = kGroups[gi];
     if (!rm::chain_supported(np, G)) continue;
     int n = 0;
@@ -125,7 +138,7 @@ int rm_grid_create(int nx, int ny, const double* t1x_col, const double* t1x_row,
   g->scratch_clusters = maxc;
   if ((e = cudaMalloc(&g->d_gens, sizeof(double) * tab.size())) != cudaSuccess ||
       (e = cudaMemcpy(g->d_gens, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice)) != cudaSuccess ||
-      (e = cudaMalloc(&g->d_scratch, sizeof(double) * 3 * (size_t)np * np * maxc)) != cudaSuccess ||
+      (e = cudaMalloc(&g->d_scratch, sizeof(double) * scratch_per_cluster * maxc)) != cudaSuccess ||
       (e = cudaMalloc(&g->d_counter, sizeof(int))) != cudaSuccess ||
       (e = cudaMalloc(&g->d_fail, sizeof(int))) != cudaSuccess ||
       (e = cudaMemset(g->d_fail, 0, sizeof(int))) != cudaSuccess ||
@@ -176,7 +189,10 @@ int rm_apply_batched(const rm_grid* g, int which, int batch, const double* d_dt,
   a.v_stride = v_stride;
   a.out = d_out;
   a.out_stride = out_stride;
-  RM_CUDA(rm::launch_apply(g->np, a, batch, (cudaStream_t)stream), "rm_apply_batched");
+  if (rm::big_supported(g->np))
+    RM_CUDA(rm::launch_apply_big(g->np, a, batch, (cudaStream_t)stream), "rm_apply_batched");
+  else
+    RM_CUDA(rm::launch_apply(g->np, a, batch, (cudaStream_t)stream), "rm_apply_batched");
   return RM_OK;
 }
 
@@ -215,6 +231,31 @@ int rm_sweep_run(rm_grid* g, const rm_sweep* sw, void* stream) {
   if (!sw->d_counters) return fail(RM_EINVAL, "rm_sweep_run: d_counters is required");
   if (!(sw->rel_tol > 0)) return fail(RM_EINVAL, "relative tolerance must be positive");
   if (sw->precond && !g->d_dm) return fail(RM_EINVAL, "rm_sweep_run: precond=1 needs rm_grid_set_tau first");
+  if (rm::big_supported(g->np)) {
+    if (sw->group > 0 && sw->group != rm::big_group(g->np))
+      return fail(RM_EUNSUP, "rm_sweep_run: the large-grid kernel uses a fixed cluster size");
+    const int gi_big = rm::big_group(g->np) == 4 ? 2 : 4;
+    rm::ChainArgs a;
+    a.sw = *sw;
+    a.nx = g->nx;
+    a.ny = g->ny;
+    a.cm = g->cm;
+    a.gens = g->d_gens;
+    a.scratch = g->d_scratch;
+    a.chain_counter = g->d_counter;
+    a.fail = g->d_fail;
+    a.fail_info = g->d_fail_info;
+    a.timing = g->d_timing;
+    a.dm = g->d_dm;
+    a.dk = g->d_dk;
+    a.tabx = g->d_tab;
+    a.taby = g->d_tab ? g->d_tab + (2 * g->np + 8) : nullptr;
+    cudaStream_t stb = (cudaStream_t)stream;
+    RM_CUDA(cudaMemsetAsync(g->d_counter, 0, sizeof(int), stb), "rm_sweep_run: counter reset");
+    RM_CUDA(rm::launch_big(g->np, a, std::min(g->max_clusters[gi_big], g->scratch_clusters), stb),
+            "rm_sweep_run: launch (large grid)");
+    return RM_OK;
+  }
   int G = sw->group > 0 ? sw->group : choose_group(g, sw->nchains);
   if (!rm::chain_supported(g->np, G))
     return fail(RM_EUNSUP, "rm_sweep_run: group size " + std::to_string(G) + " unsupported for order " +

@@ -51,6 +51,12 @@ cudaError_t launch_apply(int np, const ApplyArgs& a, int batch, cudaStream_t st)
 cudaError_t launch_pcg64(const PcgArgs& a, cudaStream_t st);
 cudaError_t launch_correct(int ndof, int nc, int m, double* u, int64_t us, const double* uc, int64_t ucs,
                            cudaStream_t st);
+bool big_supported(int np);
+int big_group(int np);
+size_t big_scratch_doubles_per_cluster(int np);
+cudaError_t launch_big(int np, const ChainArgs& a, int max_clusters, cudaStream_t st);
+cudaError_t big_max_clusters(int np, int* out);
+cudaError_t launch_apply_big(int np, const ApplyArgs& a, int batch, cudaStream_t st);
 cudaError_t launch_diff_sqnorm(int64_t n, const double* a, const double* b, double* out, cudaStream_t st);
 
 }  // namespace rm

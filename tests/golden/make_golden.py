@@ -200,6 +200,24 @@ def reduced():
     save("reduced.npz", **out)
 
 
+def big():
+    """Full spatial sizes of BASELINE configs 3 (255^2) and 4 (511^2) at reduced Nt; U stored at a few points."""
+    out = {}
+    runs = [("c3", "cfg3", dict(Nt=32), None, (16, 32)), ("c4", "cfg4", dict(Nt=16), None, (8, 16))]
+    for tag, name, kw, lv, keep in runs:
+        case = make_case(name, **kw)
+        spec = ref_spec(case)
+        t = time.perf_counter()
+        opts = MgritOptions(m=case.m, max_levels=lv, halt_tol=case.halt_tol, cg_rel_tol=case.cg_rel_tol)
+        U, tr = solve(spec, opts)
+        print(f"{name} {kw}: {tr.iterations} its in {time.perf_counter() - t:.1f}s")
+        out[f"{tag}_keep"] = np.array(keep)
+        out[f"{tag}_U"] = U[list(keep)]
+        out[f"{tag}_norms"] = np.linalg.norm(U, axis=1)
+        out.update(trace_arrays(tag, tr))
+    save("big.npz", **out)
+
+
 def pcg64():
     rng = np.random.default_rng(0)
     st = rng.bit_generator.state["state"]
@@ -214,7 +232,7 @@ def pcg64():
 if __name__ == "__main__":
     which = sys.argv[1:] or ["operators", "cg", "stepper", "mgrit_small", "pcg64", "cfg1", "reduced"]
     fns = {"operators": operators, "cg": cg_cases, "stepper": stepper_cases, "mgrit_small": mgrit_small,
-           "pcg64": pcg64, "cfg1": cfg1, "reduced": reduced}
+           "pcg64": pcg64, "cfg1": cfg1, "reduced": reduced, "big": big}
     for w in which:
         t = time.perf_counter()
         fns[w]()

@@ -1,0 +1,75 @@
+"""GPU parity for the large-grid kernels (operand streamed from L2; BASELINE configs 3 and 4 sizes)."""
+
+import numpy as np
+import pytest
+
+from oracle import riesz_oracle as O
+from paper_1805_06688_b200 import assembly
+from paper_1805_06688_b200.configs import make_case
+from paper_1805_06688_b200.krylov import CgOptions
+from paper_1805_06688_b200.mesh import SpatialGrid, uniform_temporal
+from paper_1805_06688_b200.mgrit import MgritOptions, solve
+from paper_1805_06688_b200.stepper import Discretization, ProblemSpec
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300)
+
+
+GRIDS = [(256, 256, 0.75, 0.75, 1.0, 0.5), (200, 150, 0.6, 0.8, 1.0, 2.0), (512, 512, 0.55, 0.9, 1.0, 1.0)]
+
+
+@pytest.mark.parametrize("mx,my,b,g,kx,ky", GRIDS)
+def test_big_apply_matches_oracle(mx, my, b, g, kx, ky):
+    grid = SpatialGrid(mx, my)
+    ops = O.Operators(O.Grid(mx, my), kx, ky, b, g)
+    V = np.random.default_rng(0).standard_normal((2, grid.ndof))
+    mass = assembly.mass_operator(grid)
+    sx = assembly.stiffness_operator_x(grid, b)
+    sy = assembly.stiffness_operator_y(grid, g)
+    for k in range(2):
+        assert rel(mass.apply(V[k]), ops.mass(V[k])) <= 1e-13
+        assert rel(sx.apply(V[k]), ops.sx(V[k])) <= 1e-13
+        assert rel(sy.apply(V[k]), ops.sy(V[k])) <= 1e-13
+        for sign in (1, -1):
+            op = assembly.combined_step_operator(mass, sx, sy, kx, ky, 0.01, sign)
+            assert rel(op.apply(V[k]), ops.step_apply(0.01, sign, V[k])) <= 1e-13
+
+
+@pytest.mark.parametrize("pre", ["none", "tau"])
+@pytest.mark.parametrize("mx,my,b,g,kx,ky", GRIDS[:2])
+def test_big_propagate_matches_oracle(mx, my, b, g, kx, ky, pre):
+    grid = SpatialGrid(mx, my)
+    spec = ProblemSpec(grid, uniform_temporal(1.0, 4), kx, ky, b, g, lambda x, y, t: 0 * x, lambda x, y: 0 * x)
+    disc = Discretization(spec, cg_opts=CgOptions(rel_tol=1e-12, preconditioner=pre))
+    st = O.Stepper(O.Problem(O.Grid(mx, my), spec.tmesh.points, kx, ky, b, g, spec.source, spec.initial),
+                   rel_tol=1e-12)
+    V = np.random.default_rng(1).random((3, grid.ndof))
+    for dt in (1.0 / 1024, 1.0 / 16):
+        got = disc.propagate(dt, V)
+        for k in range(3):
+            assert rel(got[k], st.propagate(dt, V[k])) <= 1e-10
+
+
+@pytest.mark.parametrize("pre", ["none", "tau"])
+@pytest.mark.parametrize("tag,name,nt", [("c3", "cfg3", 32), ("c4", "cfg4", 16)])
+def test_big_mgrit_matches_reference(golden, tag, name, nt, pre):
+    try:
+        g = golden("big.npz")
+    except FileNotFoundError:
+        pytest.skip("big.npz not generated")
+    case = make_case(name, Nt=nt)
+    opts = MgritOptions(m=case.m, halt_tol=case.halt_tol, cg_rel_tol=case.cg_rel_tol, cg_preconditioner=pre)
+    U, trace = solve(ProblemSpec(**case.problem_kwargs()), opts)
+    ref_res = g[f"{tag}_res"]
+    assert trace.iterations == len(ref_res) - 1
+    assert np.array_equal(np.array(trace.spatial_solves), g[f"{tag}_solves"])
+    assert trace.residual_norms[0] == pytest.approx(float(ref_res[0]), rel=1e-10)
+    keep = list(g[f"{tag}_keep"])
+    R = g[f"{tag}_U"]
+    for k, n in enumerate(keep):
+        assert rel(U[n], R[k]) <= 1e-10
+    norms = np.linalg.norm(U, axis=1)
+    assert np.allclose(norms, g[f"{tag}_norms"], rtol=1e-10, atol=0)
