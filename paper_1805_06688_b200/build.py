@@ -57,6 +57,8 @@ def nvcc() -> str:
 def build(force: bool = False, verbose: bool = False, timing: bool = False) -> str:
     """Build the library; ``timing=True`` builds a phase-timing debug variant next to it."""
     out = lib_path() if not timing else lib_path().replace(".so", "_timing.so")
+    if os.environ.get("RM_LIB_OUT"):
+        out = os.environ["RM_LIB_OUT"]
     if not force and not is_stale():
         return out
     os.makedirs(LIBDIR, exist_ok=True)
@@ -64,6 +66,7 @@ def build(force: bool = False, verbose: bool = False, timing: bool = False) -> s
     for src in SOURCES:
         obj = os.path.join(LIBDIR, src.replace(".cu", ".o"))
         extra = ["-DRM_TIMING"] if timing else []
+        extra += [f"-D{d}" for d in os.environ.get("RM_DEFINES", "").split(",") if d]
         cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(REPO, "include"), "-I", CSRC, "-c",
                os.path.join(CSRC, src), "-o", obj]
         res = subprocess.run(cmd, capture_output=True, text=True)

@@ -59,6 +59,10 @@ struct Cfg {
   static constexpr int ST = 2 * NP + 8;  // sine table length (>= 2(n+1))
   static constexpr size_t SMEM = sizeof(double) * (VT + 6 * GL + RED + XS + 2 * ST) + 64;
   static constexpr size_t APPLY_SMEM = sizeof(double) * (VT + 6 * GL);
+  // Row permutation: unit row ur holds rows 32*(ur/2) + (ur%2) + 2t, t < 16 (one parity inside a
+  // 32-row block) so that the DST even/odd folding gives every MMA fragment a single K operand.
+  static constexpr bool FOLD = UR >= 2;
+  static constexpr int HALF = NP / 2;
   static_assert(G * CU == U, "CTA tiling");
   static_assert(CR % WR == 0 && CC % WC == 0, "warp tiling");
   static_assert(WARPS >= 1 && WARPS <= 16, "warps");
@@ -74,6 +78,15 @@ __device__ __forceinline__ void dmma(double (&c)[4], double a0, double a1, doubl
 template <class C>
 __device__ __forceinline__ int vt_idx(int j, int i) {
   return (j + 1) * C::S + i + 2;
+}
+
+// row of local row r (0..15) of unit row ur
+template <class C>
+__device__ __forceinline__ int prow(int ur, int r) {
+  if constexpr (C::FOLD)
+    return 32 * (ur >> 1) + (ur & 1) + 2 * r;
+  else
+    return 16 * ur + r;
 }
 
 // acc[mr][nf][e] = X + Y over the warp's units (see file comment).
@@ -92,16 +105,19 @@ __device__ __forceinline__ void matvec(const double* __restrict__ Vt, const doub
     for (int seg = 0; seg < 3; ++seg) {
       const int delta = seg == 0 ? 0 : (seg == 1 ? 1 : -1);
       const double* tab = gens + seg * C::GL + C::NP + 16 * ucol + gq - tig;
-      const double* ar[C::WR];
+      const double* ar[C::WR][2];
 #pragma unroll
-      for (int mr = 0; mr < C::WR; ++mr) ar[mr] = Vt + vt_idx<C>(16 * (urow + mr) + gq + delta, tig);
+      for (int mr = 0; mr < C::WR; ++mr) {
+        ar[mr][0] = Vt + vt_idx<C>(prow<C>(urow + mr, gq) + delta, tig);
+        ar[mr][1] = Vt + vt_idx<C>(prow<C>(urow + mr, gq + 8) + delta, tig);
+      }
 #pragma unroll 4
       for (int k0 = 0; k0 < kx_end; k0 += 4) {
         double a[C::WR][2], b[C::NF];
 #pragma unroll
         for (int mr = 0; mr < C::WR; ++mr) {
-          a[mr][0] = ar[mr][k0];
-          a[mr][1] = ar[mr][k0 + 8 * C::S];
+          a[mr][0] = ar[mr][0][k0];
+          a[mr][1] = ar[mr][1][k0];
         }
 #pragma unroll
         for (int nf = 0; nf < C::NF; ++nf) b[nf] = tab[8 * nf - k0];
@@ -116,15 +132,21 @@ __device__ __forceinline__ void matvec(const double* __restrict__ Vt, const doub
 #pragma unroll 1
     for (int seg = 0; seg < 3; ++seg) {
       const int delta = seg == 0 ? 0 : (seg == 1 ? 1 : -1);
-      const double* tab = gens + (3 + seg) * C::GL + C::NP + gq - tig;
+      const double* tab = gens + (3 + seg) * C::GL + C::NP - tig;
       const double* br = Vt + vt_idx<C>(tig, 16 * ucol + gq + delta);
+      int ra[C::WR], rb[C::WR];
+#pragma unroll
+      for (int mr = 0; mr < C::WR; ++mr) {
+        ra[mr] = prow<C>(urow + mr, gq);
+        rb[mr] = prow<C>(urow + mr, gq + 8);
+      }
 #pragma unroll 4
       for (int l0 = 0; l0 < ky_end; l0 += 4) {
         double a[C::WR][2], b[C::NF];
 #pragma unroll
         for (int mr = 0; mr < C::WR; ++mr) {
-          a[mr][0] = tab[16 * (urow + mr) - l0];
-          a[mr][1] = tab[16 * (urow + mr) + 8 - l0];
+          a[mr][0] = tab[ra[mr] - l0];
+          a[mr][1] = tab[rb[mr] - l0];
         }
 #pragma unroll
         for (int nf = 0; nf < C::NF; ++nf) b[nf] = br[l0 * C::S + 8 * nf];
@@ -145,21 +167,31 @@ __device__ __forceinline__ void matvec(const double* __restrict__ Vt, const doub
 //        out^T[i][j] = sum_k Sx[i][k] V^T[k][j] so that the table is again the A operand; the
 //        warp tile is (16 i) x (16*WC j) with j in the CTA's own band.
 // ----------------------------------------------------------------------------
+// Folding (n = NP-1, N1 = NP): for the DST-I, S[a][N1-2-b] = (-1)^a S[a][b] (0-based), so with
+// u_b = v_b + v_{NP-2-b} (b < HALF-1), u_{HALF-1} = v_{HALF-1}, w_b = v_b - v_{NP-2-b}:
+//   outputs a even (alpha = a+1 odd):  sum_{b<HALF} S[a][b] u_b
+//   outputs a odd  (alpha even):       sum_{b<HALF-1} S[a][b] w_b
+// The folded vector is stored in place as u at [0, HALF) and w at [HALF, NP-1) (entry NP-1 is the
+// zero padding): half the contraction length.  fold_rows/fold_cols do it for a tile.
+
+// y-direction DST, normal mapping: out[j][i] = sum_l Sy[j][l] V[l][i]  (V folded along rows if fold)
 template <class C>
 __device__ __forceinline__ void dst_y(const double* __restrict__ Vt, const double* __restrict__ tab, int L,
                                       double (&acc)[C::WR][C::NF][4], int urow, int ucol, int gq, int tig,
-                                      int k_end) {
+                                      int k_end, bool fold) {
   static_assert(C::WR == 1, "DST stages assume one unit row per warp");
 #pragma unroll
   for (int nf = 0; nf < C::NF; ++nf)
 #pragma unroll
     for (int e = 0; e < 4; ++e) acc[0][nf][e] = 0.0;
-  const int ja = 16 * urow + gq + 1, jb = ja + 8;
+  const int ja = prow<C>(urow, gq) + 1, jb = prow<C>(urow, gq + 8) + 1;  // alpha = j + 1
   int ia = (ja * (tig + 1)) % L, ib = (jb * (tig + 1)) % L;
   const int sa = (4 * ja) % L, sb = (4 * jb) % L;
-  const double* br = Vt + vt_idx<C>(tig, 16 * ucol + gq);
+  const int rowoff = (fold && (urow & 1)) ? C::HALF : 0;  // odd unit rows: alpha even -> w half
+  const int kend = fold ? C::HALF : k_end;
+  const double* br = Vt + vt_idx<C>(tig + rowoff, 16 * ucol + gq);
 #pragma unroll 4
-  for (int l0 = 0; l0 < k_end; l0 += 4) {
+  for (int l0 = 0; l0 < kend; l0 += 4) {
     const double a0 = tab[ia], a1 = tab[ib];
     double b[C::NF];
 #pragma unroll
@@ -173,30 +205,82 @@ __device__ __forceinline__ void dst_y(const double* __restrict__ Vt, const doubl
   }
 }
 
+// output alpha (1-based DST index) of transposed-stage row m (0..NP-1)
+template <class C>
+__device__ __forceinline__ int fold_alpha(int m, bool fold) {
+  if (!fold) return m + 1;
+  return m < C::HALF ? 2 * m + 1 : 2 * (m - C::HALF) + 2;
+}
+
+// x-direction DST, transposed mapping: out^T[i][j] = sum_k Sx[i][k] V[j][k], j over the rows of
+// units tn .. tn+WC-1 (V folded along columns if fold)
 template <class C>
 __device__ __forceinline__ void dst_xT(const double* __restrict__ Vt, const double* __restrict__ tab, int L,
                                        double (&acc)[C::WR][C::NF][4], int tm, int tn, int gq, int tig,
-                                       int k_end) {
+                                       int k_end, bool fold) {
 #pragma unroll
   for (int nf = 0; nf < C::NF; ++nf)
 #pragma unroll
     for (int e = 0; e < 4; ++e) acc[0][nf][e] = 0.0;
-  const int xa = 16 * tm + gq + 1, xb = xa + 8;
+  const int xa = fold_alpha<C>(16 * tm + gq, fold), xb = fold_alpha<C>(16 * tm + gq + 8, fold);
   int ia = (xa * (tig + 1)) % L, ib = (xb * (tig + 1)) % L;
   const int sa = (4 * xa) % L, sb = (4 * xb) % L;
-  const double* br = Vt + vt_idx<C>(16 * tn + gq, tig);
+  const int coloff = (fold && 16 * tm >= C::HALF) ? C::HALF : 0;
+  const int kend = fold ? C::HALF : k_end;
+  const double* br[C::NF];
+#pragma unroll
+  for (int nf = 0; nf < C::NF; ++nf) br[nf] = Vt + vt_idx<C>(prow<C>(tn + (nf >> 1), 8 * (nf & 1) + gq), tig + coloff);
 #pragma unroll 4
-  for (int k0 = 0; k0 < k_end; k0 += 4) {
+  for (int k0 = 0; k0 < kend; k0 += 4) {
     const double a0 = tab[ia], a1 = tab[ib];
     double b[C::NF];
 #pragma unroll
-    for (int nf = 0; nf < C::NF; ++nf) b[nf] = br[8 * nf * C::S + k0];
+    for (int nf = 0; nf < C::NF; ++nf) b[nf] = br[nf][k0];
 #pragma unroll
     for (int nf = 0; nf < C::NF; ++nf) dmma(acc[0][nf], a0, a1, b[nf]);
     ia += sa;
     ia -= ia >= L ? L : 0;
     ib += sb;
     ib -= ib >= L ? L : 0;
+  }
+}
+
+// fold the columns of rows {prow(ur, t)} for unit rows [ur0, ur0+nur) (in place, see above)
+template <class C>
+__device__ __forceinline__ void fold_cols(double* Vt, int ur0, int nur, int tid) {
+  constexpr int H = C::HALF, NT = H / 2;  // pair tasks (c, H-2-c) per row
+  const int ntask = nur * 16 * NT;
+  for (int t = tid; t < ntask; t += C::THREADS) {
+    const int rr = t / NT, cc = t % NT;
+    double* row = Vt + vt_idx<C>(prow<C>(ur0 + rr / 16, rr % 16), 0);
+    const int c1 = cc, c2 = H - 2 - cc;
+    const double a1 = row[c1], b1 = row[C::NP - 2 - c1], a2 = row[c2], b2 = row[C::NP - 2 - c2];
+    row[c1] = a1 + b1;
+    row[H + c1] = a1 - b1;
+    if (c2 != c1) {
+      row[c2] = a2 + b2;
+      row[H + c2] = a2 - b2;
+    }
+  }
+}
+
+// fold the rows of the whole tile (all columns, in place)
+template <class C>
+__device__ __forceinline__ void fold_rows(double* Vt, int tid) {
+  constexpr int H = C::HALF, NT = H / 2;
+  const int ntask = C::NP * NT;
+  for (int t = tid; t < ntask; t += C::THREADS) {
+    const int i = t % C::NP, cc = t / C::NP;
+    const int c1 = cc, c2 = H - 2 - cc;
+    double* col = Vt + vt_idx<C>(0, i);
+    const double a1 = col[c1 * C::S], b1 = col[(C::NP - 2 - c1) * C::S];
+    const double a2 = col[c2 * C::S], b2 = col[(C::NP - 2 - c2) * C::S];
+    col[c1 * C::S] = a1 + b1;
+    col[(H + c1) * C::S] = a1 - b1;
+    if (c2 != c1) {
+      col[c2 * C::S] = a2 + b2;
+      col[(H + c2) * C::S] = a2 - b2;
+    }
   }
 }
 
@@ -268,23 +352,31 @@ __device__ __forceinline__ void bcast_setup(Bcast<C>& b, double* Vt, uint64_t* m
 }
 
 // Region of Vt owned by CTA `rank`: nseg segments of seg_bytes starting at seg_off(t).
+// A contiguous band when the CTA owns an even number of unit rows (or no permutation is used);
+// otherwise 16 row segments (full rows, or half rows when two CTAs share a unit row).
+template <class C>
+struct BcastShape {
+  static constexpr bool BAND = (C::G <= C::UR) && (!C::FOLD || (C::CR % 2 == 0));
+  static constexpr int NSEG = BAND ? 1 : 16;
+  static constexpr uint32_t SEG_BYTES = BAND ? sizeof(double) * C::CR * 16 * C::S
+                                             : (C::G <= C::UR ? sizeof(double) * C::S : sizeof(double) * C::CC * 16);
+};
+
 template <class C>
 __device__ __forceinline__ uint32_t bcast_seg_off(int rank, int t) {
-  if constexpr (C::G <= C::UR) {
+  using SH = BcastShape<C>;
+  if constexpr (SH::BAND) {
     return static_cast<uint32_t>(sizeof(double) * (rank * C::CR * 16 + 1) * C::S);
+  } else if constexpr (C::G <= C::UR) {
+    const int r = prow<C>(rank * C::CR, t);
+    return static_cast<uint32_t>(sizeof(double) * (r + 1) * C::S);
   } else {
     constexpr int per = C::G / C::UR;
-    const int r = 16 * (rank / per) + t;
+    const int r = prow<C>(rank / per, t);
     const int c0 = (rank % per) * C::CC * 16;
     return static_cast<uint32_t>(sizeof(double) * ((r + 1) * C::S + c0 + 2));
   }
 }
-template <class C>
-struct BcastShape {
-  static constexpr int NSEG = (C::G <= C::UR) ? 1 : 16;
-  static constexpr uint32_t SEG_BYTES =
-      (C::G <= C::UR) ? sizeof(double) * C::CR * 16 * C::S : sizeof(double) * C::CC * 16;
-};
 
 // Call after this CTA's threads wrote their elements of Vt (own band only).
 template <class C>

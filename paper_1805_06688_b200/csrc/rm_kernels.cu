@@ -43,6 +43,8 @@ struct Ctx {
   int tid, lane, warp, gq, tig, rank;
   int urow, ucol;  // first unit (row, col) of this warp
   int tm, tn;      // transposed DST stage: unit column (m) and first unit row (n) of this warp
+  int own_ur0, own_nur;  // unit rows owned by this CTA (x-fold of the DST)
+  int tm_fold;           // transposed-stage m unit when the x-direction DST is folded
 };
 
 #define RM_FOR_ELEM                                \
@@ -52,7 +54,7 @@ struct Ctx {
 
 template <class C>
 __device__ __forceinline__ int elem_row(const Ctx<C>& c, int mr, int e) {
-  return 16 * (c.urow + mr) + c.gq + 8 * (e >> 1);
+  return prow<C>(c.urow + mr, c.gq + 8 * (e >> 1));
 }
 template <class C>
 __device__ __forceinline__ int elem_col(const Ctx<C>& c, int nf, int e) {
@@ -101,12 +103,9 @@ __device__ __forceinline__ int elem_xidx(const Ctx<C>& c, int mr, int nf, int e)
 // element (row j, col i) held by (nf, e) of the transposed DST-x stage
 template <class C>
 __device__ __forceinline__ int elemT_row(const Ctx<C>& c, int nf, int e) {
-  return 16 * c.tn + 8 * nf + 2 * c.tig + (e & 1);
+  return prow<C>(c.tn + (nf >> 1), 8 * (nf & 1) + 2 * c.tig + (e & 1));
 }
-template <class C>
-__device__ __forceinline__ int elemT_col(const Ctx<C>& c, int e) {
-  return 16 * c.tm + c.gq + 8 * (e >> 1);
-}
+
 
 // Shared state of one chain kernel instance (per CTA).
 template <class C>
@@ -120,8 +119,12 @@ struct Smem {
   double* red_peer[C::G];
 };
 
-// z = P^{-1} r for the tau preconditioner: Vt <- r; T1 = R Sx; T2 = Sy T1 * dinv; T3 = T2 Sx; z = Sy T3.
-// Precondition: every CTA of the group finished reading Vt.  Result z in acc (normal mapping).
+// z = P^{-1} r for the tau preconditioner: T1 = R Sx; T2 = Sy T1 * dinv; T3 = T2 Sx; z = Sy T3.
+// The x-direction stages read only this CTA's own rows (transposed mapping), so their inputs are
+// written locally without any exchange; only the y-stage inputs (T1, T3) are broadcast.  A cluster
+// barrier after each broadcast guarantees every outgoing bulk copy has landed before the own band is
+// folded in place.  Precondition: every CTA finished reading its operand tile and nobody reads this
+// CTA's own rows any more.  Result z in acc (normal mapping).
 template <class C>
 __device__ __forceinline__ void apply_tau(const Ctx<C>& c, const Smem<C>& sm, Bcast<C>& bc,
                                           const double (&r)[C::WR][C::NF][4], double (&acc)[C::WR][C::NF][4],
@@ -135,34 +138,55 @@ __device__ __forceinline__ void apply_tau(const Ctx<C>& c, const Smem<C>& sm, Bc
   } P{timing};
 #endif
   RM_T0();
+#ifdef RM_NO_FOLD
+  const bool fold_x = false, fold_y = false;
+#else
+  const bool fold_x = C::FOLD && nx == C::NP - 1, fold_y = C::FOLD && ny == C::NP - 1;
+#endif
   RM_FOR_ELEM {
     const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
     if (j < ny && i < nx) Vt[vt_idx<C>(j, i)] = r[mr][nf][e];
   }
-  bcast_band<C>(bc, c.rank, c.tid);
+  __syncthreads();
   RM_T(8);
+  const int tm = fold_x ? c.tm_fold : c.tm;
 #pragma unroll 1
   for (int pass = 0; pass < 2; ++pass) {
-    // x-direction (transposed mapping)
-    dst_xT<C>(Vt, sm.tabx, Lx, acc, c.tm, c.tn, c.gq, c.tig, kx_end);
+    if constexpr (C::G > C::UR) {
+      // two CTAs share each own row (column halves): exchange the halves, and let every outgoing
+      // copy land before the rows are folded in place
+      bcast_band<C>(bc, c.rank, c.tid);
+      group_sync<C::G>();
+    }
+    // x-direction (transposed mapping) on the CTA's own rows
+    if (fold_x) {
+      fold_cols<C>(Vt, c.own_ur0, c.own_nur, c.tid);
+      __syncthreads();
+    }
+    dst_xT<C>(Vt, sm.tabx, Lx, acc, tm, c.tn, c.gq, c.tig, kx_end, fold_x);
+    __syncthreads();
     RM_T(9);
-    group_sync<C::G>();
     RM_FOR_ELEM {
-      const int j = elemT_row<C>(c, nf, e), i = elemT_col<C>(c, e);
+      const int j = elemT_row<C>(c, nf, e), i = fold_alpha<C>(16 * tm + c.gq + 8 * (e >> 1), fold_x) - 1;
       if (j < ny && i < nx) Vt[vt_idx<C>(j, i)] = acc[mr][nf][e];
     }
     bcast_band<C>(bc, c.rank, c.tid);
+    if (fold_y) {
+      if constexpr (C::G > 1) group_sync<C::G>();  // all outgoing copies of the own band completed
+      fold_rows<C>(Vt, c.tid);
+      __syncthreads();
+    }
     RM_T(10);
-    // y-direction (normal mapping)
-    dst_y<C>(Vt, sm.taby, Ly, acc, c.urow, c.ucol, c.gq, c.tig, ky_end);
+    // y-direction (normal mapping) over all rows
+    dst_y<C>(Vt, sm.taby, Ly, acc, c.urow, c.ucol, c.gq, c.tig, ky_end, fold_y);
     RM_T(11);
     if (pass == 1) break;
-    group_sync<C::G>();
+    group_sync<C::G>();  // every CTA done reading its tile before peers push the next band
     RM_FOR_ELEM {
       const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
       if (j < ny && i < nx) Vt[vt_idx<C>(j, i)] = acc[mr][nf][e] * __ldcg(dinv + elem_sidx<C>(c, mr, nf, e));
     }
-    bcast_band<C>(bc, c.rank, c.tid);
+    __syncthreads();
     RM_T(12);
   }
 }
@@ -210,6 +234,15 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
     constexpr int tcols = C::CR / C::WC > 0 ? C::CR / C::WC : 1;
     c.tm = c0 + c.warp / tcols;
     c.tn = r0 + (c.warp % tcols) * C::WC;
+    c.own_ur0 = r0;
+    c.own_nur = C::CR;
+    c.tm_fold = c.tm;
+    if constexpr (C::G > C::UR) {
+      // two CTAs share a unit row (column halves): with the fold, output column i = alpha - 1 comes
+      // from m = i/2 (i even) or HALF + i/2 (i odd), so take both halves' m units of own columns
+      const int w = c.warp / tcols;
+      c.tm_fold = w < C::CC / 2 ? c0 / 2 + w : C::UR / 2 + c0 / 2 + (w - C::CC / 2);
+    }
   }
 
   int* sched_peer[C::G];

@@ -25,7 +25,7 @@ def fmv(nx, ny):
 
 
 def fpc(nx, ny):
-    return 4 * nx * ny * (nx + ny) + nx * ny
+    return 2 * nx * ny * (nx + ny) + 5 * nx * ny
 
 
 def main():
