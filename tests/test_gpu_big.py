@@ -53,13 +53,19 @@ def test_big_propagate_matches_oracle(mx, my, b, g, kx, ky, pre):
             assert rel(got[k], st.propagate(dt, V[k])) <= 1e-10
 
 
-@pytest.mark.parametrize("pre", ["none", "tau"])
-@pytest.mark.parametrize("tag,name,nt", [("c3", "cfg3", 32), ("c4", "cfg4", 16)])
-def test_big_mgrit_matches_reference(golden, tag, name, nt, pre):
+@pytest.mark.parametrize("tag,name,nt,pre,fixture", [
+    ("c3", "cfg3", 32, "none", "big.npz"),
+    ("c3", "cfg3", 32, "tau", "big.npz"),
+    ("c4", "cfg4", 16, "none", "big.npz"),
+    # at 511^2 the reference's own 1e-12 inner solves are ~2e-10 from the converged answer; the
+    # preconditioned path is closer to it, so it is checked against the reference run at 1e-14
+    ("c4t", "cfg4", 16, "tau", "big_tight.npz"),
+])
+def test_big_mgrit_matches_reference(golden, tag, name, nt, pre, fixture):
     try:
-        g = golden("big.npz")
+        g = golden(fixture)
     except FileNotFoundError:
-        pytest.skip("big.npz not generated")
+        pytest.skip(f"{fixture} not generated")
     case = make_case(name, Nt=nt)
     opts = MgritOptions(m=case.m, halt_tol=case.halt_tol, cg_rel_tol=case.cg_rel_tol, cg_preconditioner=pre)
     U, trace = solve(ProblemSpec(**case.problem_kwargs()), opts)
