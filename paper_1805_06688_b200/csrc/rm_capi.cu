@@ -196,20 +196,28 @@ int rm_apply_batched(const rm_grid* g, int which, int batch, const double* d_dt,
   return RM_OK;
 }
 
+// Relative time of one chain step on a cluster of G CTAs (measured on B200, tools/group_sweep.py,
+// cfg2 127^2: G=2 1.29 ms, G=4 0.83, G=8 0.62, G=16 0.97 per PCG step; 16-CTA clusters have 4-warp
+// CTAs and 15-peer exchanges).  Lower is faster; 0 = not available.
+static double group_step_cost(int np, int G) {
+  switch (np) {
+    case 128: return G == 2 ? 1.0 : G == 4 ? 0.64 : G == 8 ? 0.48 : G == 16 ? 0.75 : 0.0;
+    case 64: return G == 1 ? 1.0 : G == 2 ? 0.62 : G == 4 ? 0.5 : 0.0;
+    case 32: return G == 1 ? 1.0 : G == 2 ? 0.75 : 0.0;
+    default: return G == 1 ? 1.0 : 0.0;
+  }
+}
+
 static int choose_group(const rm_grid* g, int nchains) {
-  // relative per-iteration time of one CTA holding the whole vector
-  const double t1 = 100.0 * pow(g->np / 128.0, 3.0);
   double best = 1e300;
   int best_g = 1;
   for (int gi = 0; gi < 5; ++gi) {
     const int G = kGroups[gi];
-    if (!rm::chain_supported(g->np, G) || g->max_clusters[gi] <= 0) continue;
-    const int slots = g->max_clusters[gi];
-    const double waves = ceil((double)nchains / slots);
-    const int units_per_cta = (g->np / 16) * (g->np / 16) / G;
-    const double eff = units_per_cta >= 8 ? 1.0 : 8.0 / units_per_cta * 0.6;
-    const double est = waves * (t1 / G * eff + (G > 1 ? 1.5 + 0.1 * G : 0.3));
-    if (est < best * 0.97) {
+    const double cost = group_step_cost(g->np, G);
+    if (cost <= 0.0 || !rm::chain_supported(g->np, G) || g->max_clusters[gi] <= 0) continue;
+    const int slots = std::min(g->max_clusters[gi], g->scratch_clusters);
+    const double est = ceil((double)nchains / slots) * cost;
+    if (est < best * 0.999) {
       best = est;
       best_g = G;
     }
