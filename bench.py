@@ -35,20 +35,11 @@ import numpy as np  # noqa: E402
 
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
+from paper_1805_06688_b200.flops import fmv, fpc  # noqa: E402
+
 PROFILES = os.path.join(REPO, "profiles")
 METRIC = "MGRIT fine-step space-time DOF/s (ndof*Nt / time-to-solution to 1e-8 residual)"
 UNIT = "DOF/s"
-
-
-def fmv(nx: int, ny: int) -> float:
-    """Algorithmic FLOPs of one combined-operator apply."""
-    return 2.0 * nx * nx * (3 * ny - 2) + 2.0 * ny * ny * (3 * nx - 2) + 13.0 * nx * ny
-
-
-def fpc(nx: int, ny: int) -> float:
-    """FLOPs of one tau-preconditioner application: 2 even/odd-folded DST-I contractions per direction
-    (half the dense count), the folds and the diagonal scaling."""
-    return 2.0 * nx * ny * (nx + ny) + 5.0 * nx * ny
 
 
 def dist_env():
@@ -307,7 +298,7 @@ def run_ours(args):
     k_ms = sum(a.elapsed_time(b) for _, a, b, *_ in trace)
     mvs = sum(int((after - before)[2].item()) for _, _, _, before, after, _ in trace)
     pcs = sum(int((after - before)[3].item()) for _, _, _, before, after, _ in trace)
-    flops = mvs * fmv(case.grid.nx, case.grid.ny) + pcs * fpc(case.grid.nx, case.grid.ny)
+    flops = mvs * fmv(case.grid.nx, case.grid.ny, eng.flags) + pcs * fpc(case.grid.nx, case.grid.ny)
     achieved = flops / (k_ms * 1e-3) / 1e12
     traffic, traffic_launch = ncu_traffic()
 
@@ -352,7 +343,7 @@ def run_ours(args):
                          "kernel": "chain_kernel (FP64 DMMA block-Toeplitz matvec + fused CG)",
                          "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (FP64 not in MEASURED_PEAKS.json)",
                          "traffic_launch": traffic_launch,
-                         "flops_per_apply": fmv(case.grid.nx, case.grid.ny), "applies_per_step": mvs // args.steps,
+                         "flops_per_apply": fmv(case.grid.nx, case.grid.ny, eng.flags), "applies_per_step": mvs // args.steps,
                          "flops_per_precond": fpc(case.grid.nx, case.grid.ny),
                          "precond_applies_per_step": pcs // args.steps,
                          "kernel_ms_per_step": k_ms / args.steps},

@@ -160,6 +160,14 @@ RM_API int rm_grid_set_tau(rm_grid* grid, const double* dm, const double* dk);
 RM_API int rm_fail_info(rm_grid* grid, int* code, int* n, int64_t* iterations, double* residual_norm);
 RM_API int rm_fail_reset(rm_grid* grid, void* stream);
 
+/*
+ * Execution flags chosen for a grid (no reference counterpart; informational):
+ * bit 0 / bit 1 = the off-diagonal x / y Toeplitz segments of the matvec run merged
+ * (T2 first column == first row shifted by one, as for the Riesz stiffness, assembly.py:239-249),
+ * which cuts the matvec from 12 n^3 to 8 n^3 FLOPs.  Returns the flags, or -1 for a null grid.
+ */
+RM_API int rm_grid_flags(const rm_grid* grid);
+
 /* Debug: per-phase cycle counters of CTA 0 (filled only by -DRM_TIMING builds). */
 RM_API int rm_debug_timing(rm_grid* grid, long long* out16);
 

@@ -62,6 +62,7 @@ EXPORTS = {
                                C.POINTER(C.c_double)]),
     "rm_fail_reset": (C.c_int, [C.c_void_p, C.c_void_p]),
     "rm_debug_timing": (C.c_int, [C.c_void_p, C.POINTER(C.c_longlong)]),
+    "rm_grid_flags": (C.c_int, [C.c_void_p]),
     "rm_correct": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
                              C.c_void_p]),
     "rm_diff_sqnorm": (C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),

@@ -10,6 +10,7 @@ with the repo snapshot (it is git-ignored, not gpurun-ignored).
 from __future__ import annotations
 
 import os
+import re
 import subprocess
 import sys
 
@@ -26,6 +27,14 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
     "-Xptxas", "-v",
 ]
+
+
+def chain_cases() -> list[tuple[int, int]]:
+    """(NP, G) chain-kernel configurations listed in rm_kernels.cu's RM_CHAIN_CASES."""
+    text = open(os.path.join(CSRC, "rm_kernels.cu")).read()
+    block = text[text.index("#define RM_CHAIN_CASES(X)"):]
+    block = block[: block.index("\n\n")]
+    return [(int(a), int(b)) for a, b in re.findall(r"X\((\d+),\s*(\d+)\)", block)]
 
 
 def lib_path() -> str:
@@ -62,18 +71,32 @@ def build(force: bool = False, verbose: bool = False, timing: bool = False) -> s
     if not force and not is_stale():
         return out
     os.makedirs(LIBDIR, exist_ok=True)
-    objs = []
+    extra = ["-DRM_TIMING"] if timing else []
+    extra += [f"-D{d}" for d in os.environ.get("RM_DEFINES", "").split(",") if d]
+    jobs = []  # (label, source, defines, object)
     for src in SOURCES:
-        obj = os.path.join(LIBDIR, src.replace(".cu", ".o"))
-        extra = ["-DRM_TIMING"] if timing else []
-        extra += [f"-D{d}" for d in os.environ.get("RM_DEFINES", "").split(",") if d]
-        cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(REPO, "include"), "-I", CSRC, "-c",
-               os.path.join(CSRC, src), "-o", obj]
-        res = subprocess.run(cmd, capture_output=True, text=True)
-        if res.returncode != 0:
-            raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr}")
+        jobs.append((src, src, [], os.path.join(LIBDIR, src.replace(".cu", ".o"))))
+    for np_, g in chain_cases():  # one translation unit per chain-kernel configuration
+        jobs.append((f"rm_kernels.cu[{np_},{g}]", "rm_kernels.cu", [f"-DRM_CASE_NP={np_}", f"-DRM_CASE_G={g}"],
+                     os.path.join(LIBDIR, f"rm_chain_{np_}_{g}.o")))
+    nproc = max(1, min(len(jobs), os.cpu_count() or 1))
+    running, objs = [], []
+    pending = list(jobs)
+    while pending or running:
+        while pending and len(running) < nproc:
+            label, src, defs, obj = pending.pop(0)
+            cmd = [nvcc(), *NVCC_FLAGS, *extra, *defs, "-I", os.path.join(REPO, "include"), "-I", CSRC, "-c",
+                   os.path.join(CSRC, src), "-o", obj]
+            running.append((label, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                                         text=True)))
+        label, obj, proc = running.pop(0)
+        _, err = proc.communicate()
+        if proc.returncode != 0:
+            for _, _, p in running:
+                p.kill()
+            raise RuntimeError(f"nvcc failed for {label}:\n{err}")
         if verbose:
-            sys.stderr.write(res.stderr)
+            sys.stderr.write(f"== {label}\n{err}")
         objs.append(obj)
     tmp = out + ".tmp"
     cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs, "-lcudart"]

@@ -39,7 +39,7 @@ struct BigCfg {
   static constexpr int XROWS = 130;
   static constexpr int YS = 148;           // y-stage row stride (== 4 mod 16)
   static constexpr int YCOLS = 144;        // C0-8 .. C0+135
-  static constexpr int STAGE = (XROWS * XS > 32 * YS ? XROWS * XS : 32 * YS);  // doubles per stage
+  static constexpr int STAGE = (XROWS * XS > 33 * YS ? XROWS * XS : 33 * YS);  // doubles per stage
   static constexpr int TE = 128 * 128;     // elements per tile
   static constexpr size_t SMEM = sizeof(double) * (6 * GL + 2 * GL + 2 * STAGE + 4 * 64 + 2 * 4 * 16) + 64;
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
@@ -86,18 +86,18 @@ __device__ __forceinline__ void cp_async_wait() {
 // ---- chunk loaders (all threads) ------------------------------------------------------
 template <class C>
 __device__ __forceinline__ void load_xchunk(double* st, const double* __restrict__ pv, int R0, int k0, int tid) {
-  // rows R0-1 .. R0+128 (130), cols k0 .. k0+31 (16 x 16B per row)
-  for (int t = tid; t < C::XROWS * 16; t += C::THREADS) {
-    const int r = t >> 4, q = t & 15;
-    cp_async16(st + r * C::XS + 2 * q, pv + pv_idx<C>(R0 - 1 + r, k0) + 2 * q);
+  // rows R0-1 .. R0+128 (130), cols k0-2 .. k0+31 (17 x 16B per row; column k0-1 for the merged segment)
+  for (int t = tid; t < C::XROWS * 17; t += C::THREADS) {
+    const int r = t / 17, q = t % 17;
+    cp_async16(st + r * C::XS + 2 * q, pv + pv_idx<C>(R0 - 1 + r, k0 - 2) + 2 * q);
   }
 }
 template <class C>
 __device__ __forceinline__ void load_ychunk(double* st, const double* __restrict__ pv, int l0, int C0, int tid) {
-  // rows l0 .. l0+31, cols C0-8 .. C0+135 (72 x 16B per row)
-  for (int t = tid; t < 32 * 72; t += C::THREADS) {
+  // rows l0-1 .. l0+31 (row l0-1 for the merged segment), cols C0-8 .. C0+135 (72 x 16B per row)
+  for (int t = tid; t < 33 * 72; t += C::THREADS) {
     const int r = t / 72, q = t % 72;
-    cp_async16(st + r * C::YS + 2 * q, pv + pv_idx<C>(l0 + r, C0 - 8) + 2 * q);
+    cp_async16(st + r * C::YS + 2 * q, pv + pv_idx<C>(l0 - 1 + r, C0 - 8) + 2 * q);
   }
 }
 
@@ -105,7 +105,7 @@ __device__ __forceinline__ void load_ychunk(double* st, const double* __restrict
 template <class C>
 __device__ __forceinline__ void big_matvec(const double* __restrict__ pv, const double* __restrict__ gens,
                                            double* stage, double (&acc)[8][4], const BigCtx& c, int kx_end,
-                                           int ky_end) {
+                                           int ky_end, int merge) {
 #pragma unroll
   for (int nf = 0; nf < 8; ++nf)
 #pragma unroll
@@ -123,10 +123,23 @@ __device__ __forceinline__ void big_matvec(const double* __restrict__ pv, const 
     const double* s = st[ch & 1];
     const int k0 = 32 * ch;
 #pragma unroll 1
-    for (int seg = 0; seg < 3; ++seg) {
+    for (int seg = 0; seg < ((merge & 1) ? 2 : 3); ++seg) {
       const int delta = seg == 0 ? 0 : (seg == 1 ? 1 : -1);
       const double* tab = gens + seg * C::GL + C::NP + c.C0 + 16 * c.wc0 + c.gq - c.tig - k0;
-      const double* ar = s + (16 * c.wr + c.gq + delta + 1) * C::XS + c.tig;
+      const double* ar = s + (16 * c.wr + c.gq + delta + 1) * C::XS + c.tig + 2;
+      if (seg == 1 && (merge & 1)) {  // T2 (V[j+1][k] + V[j-1][k-1]), see rm_device.cuh matvec
+        const double* am = s + (16 * c.wr + c.gq) * C::XS + c.tig + 1;
+#pragma unroll 4
+        for (int k = 0; k < 32; k += 4) {
+          const double a0 = ar[k] + am[k], a1 = ar[k + 8 * C::XS] + am[k + 8 * C::XS];
+          double b[8];
+#pragma unroll
+          for (int nf = 0; nf < 8; ++nf) b[nf] = tab[8 * nf - k];
+#pragma unroll
+          for (int nf = 0; nf < 8; ++nf) dmma(acc[nf], a0, a1, b[nf]);
+        }
+        continue;
+      }
 #pragma unroll 4
       for (int k = 0; k < 32; k += 4) {
         const double a0 = ar[k], a1 = ar[k + 8 * C::XS];
@@ -151,10 +164,23 @@ __device__ __forceinline__ void big_matvec(const double* __restrict__ pv, const 
     const double* s = st[ch & 1];
     const int l0 = 32 * ch;
 #pragma unroll 1
-    for (int seg = 0; seg < 3; ++seg) {
+    for (int seg = 0; seg < ((merge & 2) ? 2 : 3); ++seg) {
       const int delta = seg == 0 ? 0 : (seg == 1 ? 1 : -1);
       const double* tab = gens + (3 + seg) * C::GL + C::NP + c.R0 + 16 * c.wr + c.gq - c.tig - l0;
-      const double* br = s + c.tig * C::YS + 16 * c.wc0 + c.gq + delta + 8;
+      const double* br = s + (c.tig + 1) * C::YS + 16 * c.wc0 + c.gq + delta + 8;
+      if (seg == 1 && (merge & 2)) {  // T2 (V[l][i+1] + V[l-1][i-1])
+        const double* bm = s + c.tig * C::YS + 16 * c.wc0 + c.gq + 7;
+#pragma unroll 4
+        for (int l = 0; l < 32; l += 4) {
+          const double a0 = tab[-l], a1 = tab[8 - l];
+          double b[8];
+#pragma unroll
+          for (int nf = 0; nf < 8; ++nf) b[nf] = br[l * C::YS + 8 * nf] + bm[l * C::YS + 8 * nf];
+#pragma unroll
+          for (int nf = 0; nf < 8; ++nf) dmma(acc[nf], a0, a1, b[nf]);
+        }
+        continue;
+      }
 #pragma unroll 4
       for (int l = 0; l < 32; l += 4) {
         const double a0 = tab[-l], a1 = tab[8 - l];
@@ -189,7 +215,7 @@ __device__ __forceinline__ void big_dst_xT(const double* __restrict__ pv, const 
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
-    const double* br = st[ch & 1] + (16 * c.wc0 + c.gq + 1) * C::XS + c.tig;
+    const double* br = st[ch & 1] + (16 * c.wc0 + c.gq + 1) * C::XS + c.tig + 2;
 #pragma unroll 4
     for (int k = 0; k < 32; k += 4) {
       const double a0 = tab[ia], a1 = tab[ib];
@@ -227,7 +253,7 @@ __device__ __forceinline__ void big_dst_y(const double* __restrict__ pv, const d
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
-    const double* br = st[ch & 1] + c.tig * C::YS + 16 * c.wc0 + c.gq + 8;
+    const double* br = st[ch & 1] + (c.tig + 1) * C::YS + 16 * c.wc0 + c.gq + 8;
 #pragma unroll 4
     for (int l = 0; l < 32; l += 4) {
       const double a0 = tab[ia], a1 = tab[ib];
@@ -387,7 +413,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
           }
           group_sync<C::G>();
         }
-        big_matvec<C>(pv0, gens, stage, acc, c, kx_end, ky_end);
+        big_matvec<C>(pv0, gens, stage, acc, c, kx_end, ky_end, P.merge);
       }
       double part[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
       RM_BIG_FOR {
@@ -427,7 +453,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
           if (j < ny && i < nx) put_tile(pv0, j, i, __ldcg(x0 + j * nx + i));
         }
         group_sync<C::G>();
-        big_matvec<C>(pv0, gens, stage, acc, c, kx_end, ky_end);
+        big_matvec<C>(pv0, gens, stage, acc, c, kx_end, ky_end, P.merge);
         ++nmv;
         part[1][0] = part[1][1] = part[1][2] = part[1][3] = 0.0;
         RM_BIG_FOR {
@@ -459,7 +485,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
           }
         }
         group_sync<C::G>();
-        big_matvec<C>(pv0, gens, stage, acc, c, kx_end, ky_end);
+        big_matvec<C>(pv0, gens, stage, acc, c, kx_end, ky_end, P.merge);
         ++nmv;
         double pg[1][4] = {{0, 0, 0, 0}};
         RM_BIG_FOR {
@@ -545,7 +571,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
           its = max_iter;
           break;
         }
-        big_matvec<C>(pv0, gens, stage, acc, c, kx_end, ky_end);
+        big_matvec<C>(pv0, gens, stage, acc, c, kx_end, ky_end, P.merge);
         ++nmv;
         double p1[1][4] = {{0, 0, 0, 0}};
         RM_BIG_FOR {
@@ -620,7 +646,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
             if (j < ny && i < nx) put_tile(pv0, j, i, xs[big_fidx(c, nf, e)]);
           }
           group_sync<C::G>();
-          big_matvec<C>(pv0, gens, stage, acc, c, kx_end, ky_end);
+          big_matvec<C>(pv0, gens, stage, acc, c, kx_end, ky_end, P.merge);
           ++nmv;
           double pt[1][4] = {{0, 0, 0, 0}};
           RM_BIG_FOR {

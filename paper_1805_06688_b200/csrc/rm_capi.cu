@@ -3,6 +3,7 @@
 #include <math.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <string>
@@ -44,6 +45,7 @@ int padded_order(int nx, int ny) {
 
 struct rm_grid {
   int nx, ny, np, device;
+  int merge = 0;  // bit 0/1: off-diagonal Toeplitz block along x/y has t2(d) = t2(-1-d) (see rm_device.cuh matvec)
   double kx, ky, sx, sy, cm;
   double* d_gens = nullptr;
   double* d_scratch = nullptr;
@@ -108,6 +110,23 @@ int rm_grid_create(int nx, int ny, const double* t1x_col, const double* t1x_row,
       tab[5 * GL + idx] = fy * t2(t2y_col, t2y_row, -d);
     }
   }
+  // T2 with first column == first row shifted by one (the Riesz stiffness A2, assembly.py:239-249):
+  // the two off-diagonal segments of the matvec merge into one of length n+1 (needs t2(-n) = col[n-1])
+  auto shifted_sym = [](const double* col, const double* row, int n) {
+    if (n % 4 == 0) return false;
+    for (int d = 0; d + 1 < n; ++d)
+      if (col[d] != row[d + 1]) return false;
+    return true;
+  };
+  if (shifted_sym(t2x_col, t2x_row, nx)) {
+    g->merge |= 1;
+    tab[1 * GL + np - nx] = fx * t2x_col[nx - 1];
+  }
+  if (shifted_sym(t2y_col, t2y_row, ny)) {
+    g->merge |= 2;
+    tab[4 * GL + np - ny] = fy * t2y_col[ny - 1];
+  }
+  if (const char* m = getenv("RM_MERGE")) g->merge &= atoi(m);
   cudaError_t e;
   int maxc = 1;
   size_t scratch_per_cluster = 3 * (size_t)np * np;
@@ -167,6 +186,8 @@ int rm_grid_destroy(rm_grid* g) {
   return RM_OK;
 }
 
+int rm_grid_flags(const rm_grid* g) { return g ? g->merge : -1; }
+
 int rm_apply_batched(const rm_grid* g, int which, int batch, const double* d_dt, int sign, const double* d_v,
                      int64_t v_stride, double* d_out, int64_t out_stride, void* stream) {
   if (!g) return fail(RM_EINVAL, "rm_apply_batched: null grid");
@@ -184,6 +205,7 @@ int rm_apply_batched(const rm_grid* g, int which, int batch, const double* d_dt,
   a.kx = g->kx;
   a.ky = g->ky;
   a.gens = g->d_gens;
+  a.merge = g->merge;
   a.dt = d_dt;
   a.v = d_v;
   a.v_stride = v_stride;
@@ -249,6 +271,7 @@ int rm_sweep_run(rm_grid* g, const rm_sweep* sw, void* stream) {
     a.ny = g->ny;
     a.cm = g->cm;
     a.gens = g->d_gens;
+  a.merge = g->merge;
     a.scratch = g->d_scratch;
     a.chain_counter = g->d_counter;
     a.fail = g->d_fail;
@@ -280,6 +303,7 @@ int rm_sweep_run(rm_grid* g, const rm_sweep* sw, void* stream) {
   a.ny = g->ny;
   a.cm = g->cm;
   a.gens = g->d_gens;
+  a.merge = g->merge;
   a.scratch = g->d_scratch;
   a.chain_counter = g->d_counter;
   a.fail = g->d_fail;

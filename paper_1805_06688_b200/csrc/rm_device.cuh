@@ -89,11 +89,85 @@ __device__ __forceinline__ int prow(int ur, int r) {
     return 16 * ur + r;
 }
 
+// One x-segment: acc += sum_k tab(i-k) (V[j+d1][k] + [TWO] V[j-1][k-1]).
+template <class C, bool TWO>
+__device__ __forceinline__ void matvec_xseg(const double* __restrict__ Vt, const double* __restrict__ tab,
+                                            double (&acc)[C::WR][C::NF][4], int urow, int gq, int tig, int d1,
+                                            int k_end) {
+  const double* ar[C::WR][2];
+  const double* am[C::WR][2];
+#pragma unroll
+  for (int mr = 0; mr < C::WR; ++mr) {
+    ar[mr][0] = Vt + vt_idx<C>(prow<C>(urow + mr, gq) + d1, tig);
+    ar[mr][1] = Vt + vt_idx<C>(prow<C>(urow + mr, gq + 8) + d1, tig);
+    am[mr][0] = Vt + vt_idx<C>(prow<C>(urow + mr, gq) - 1, tig - 1);
+    am[mr][1] = Vt + vt_idx<C>(prow<C>(urow + mr, gq + 8) - 1, tig - 1);
+  }
+#pragma unroll 4
+  for (int k0 = 0; k0 < k_end; k0 += 4) {
+    double a[C::WR][2], b[C::NF];
+#pragma unroll
+    for (int mr = 0; mr < C::WR; ++mr) {
+      a[mr][0] = ar[mr][0][k0];
+      a[mr][1] = ar[mr][1][k0];
+      if constexpr (TWO) {
+        a[mr][0] += am[mr][0][k0];
+        a[mr][1] += am[mr][1][k0];
+      }
+    }
+#pragma unroll
+    for (int nf = 0; nf < C::NF; ++nf) b[nf] = tab[8 * nf - k0];
+#pragma unroll
+    for (int mr = 0; mr < C::WR; ++mr)
+#pragma unroll
+      for (int nf = 0; nf < C::NF; ++nf) dmma(acc[mr][nf], a[mr][0], a[mr][1], b[nf]);
+  }
+}
+
+// One y-segment: acc += sum_l tab(j-l) (V[l][i+d1] + [TWO] V[l-1][i-1]).
+template <class C, bool TWO>
+__device__ __forceinline__ void matvec_yseg(const double* __restrict__ Vt, const double* __restrict__ tab,
+                                            double (&acc)[C::WR][C::NF][4], int urow, int ucol, int gq, int tig,
+                                            int d1, int l_end) {
+  const double* br = Vt + vt_idx<C>(tig, 16 * ucol + gq + d1);
+  const double* bm = Vt + vt_idx<C>(tig - 1, 16 * ucol + gq - 1);
+  int ra[C::WR], rb[C::WR];
+#pragma unroll
+  for (int mr = 0; mr < C::WR; ++mr) {
+    ra[mr] = prow<C>(urow + mr, gq);
+    rb[mr] = prow<C>(urow + mr, gq + 8);
+  }
+#pragma unroll 4
+  for (int l0 = 0; l0 < l_end; l0 += 4) {
+    double a[C::WR][2], b[C::NF];
+#pragma unroll
+    for (int mr = 0; mr < C::WR; ++mr) {
+      a[mr][0] = tab[ra[mr] - l0];
+      a[mr][1] = tab[rb[mr] - l0];
+    }
+#pragma unroll
+    for (int nf = 0; nf < C::NF; ++nf) {
+      b[nf] = br[l0 * C::S + 8 * nf];
+      if constexpr (TWO) b[nf] += bm[l0 * C::S + 8 * nf];
+    }
+#pragma unroll
+    for (int mr = 0; mr < C::WR; ++mr)
+#pragma unroll
+      for (int nf = 0; nf < C::NF; ++nf) dmma(acc[mr][nf], a[mr][0], a[mr][1], b[nf]);
+  }
+}
+
 // acc[mr][nf][e] = X + Y over the warp's units (see file comment).
+// merge bit 0 (x) / bit 1 (y): the off-diagonal Toeplitz block T2 satisfies t2(d) = t2(-1-d)
+// (its first column is its first row shifted by one, assembly.py:239-249), hence
+//   T2 V[j+1] + T2^T V[j-1] = T2_ext (V[j+1][k] + V[j-1][k-1]),  k = 0..n
+// and the two off-diagonal segments become one contraction of length n+1 (12 n^3 -> 8 n^3 flops).
+// The host sets the bits only when the generators have this property exactly and n % 4 != 0, so
+// that k = n still lies inside the (zero-padded) K range [0, (n+3)&~3) of the plain segments.
 template <class C>
 __device__ __forceinline__ void matvec(const double* __restrict__ Vt, const double* __restrict__ gens,
                                        double (&acc)[C::WR][C::NF][4], int urow, int ucol, int gq, int tig,
-                                       int kx_end, int ky_end, bool do_x, bool do_y) {
+                                       int kx_end, int ky_end, bool do_x, bool do_y, int merge) {
 #pragma unroll
   for (int mr = 0; mr < C::WR; ++mr)
 #pragma unroll
@@ -101,60 +175,23 @@ __device__ __forceinline__ void matvec(const double* __restrict__ Vt, const doub
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[mr][nf][e] = 0.0;
   if (do_x) {
-#pragma unroll 1
-    for (int seg = 0; seg < 3; ++seg) {
-      const int delta = seg == 0 ? 0 : (seg == 1 ? 1 : -1);
-      const double* tab = gens + seg * C::GL + C::NP + 16 * ucol + gq - tig;
-      const double* ar[C::WR][2];
-#pragma unroll
-      for (int mr = 0; mr < C::WR; ++mr) {
-        ar[mr][0] = Vt + vt_idx<C>(prow<C>(urow + mr, gq) + delta, tig);
-        ar[mr][1] = Vt + vt_idx<C>(prow<C>(urow + mr, gq + 8) + delta, tig);
-      }
-#pragma unroll 4
-      for (int k0 = 0; k0 < kx_end; k0 += 4) {
-        double a[C::WR][2], b[C::NF];
-#pragma unroll
-        for (int mr = 0; mr < C::WR; ++mr) {
-          a[mr][0] = ar[mr][0][k0];
-          a[mr][1] = ar[mr][1][k0];
-        }
-#pragma unroll
-        for (int nf = 0; nf < C::NF; ++nf) b[nf] = tab[8 * nf - k0];
-#pragma unroll
-        for (int mr = 0; mr < C::WR; ++mr)
-#pragma unroll
-          for (int nf = 0; nf < C::NF; ++nf) dmma(acc[mr][nf], a[mr][0], a[mr][1], b[nf]);
-      }
+    const double* tab = gens + C::NP + 16 * ucol + gq - tig;
+    matvec_xseg<C, false>(Vt, tab, acc, urow, gq, tig, 0, kx_end);
+    if (merge & 1) {
+      matvec_xseg<C, true>(Vt, tab + C::GL, acc, urow, gq, tig, 1, kx_end);
+    } else {
+      matvec_xseg<C, false>(Vt, tab + C::GL, acc, urow, gq, tig, 1, kx_end);
+      matvec_xseg<C, false>(Vt, tab + 2 * C::GL, acc, urow, gq, tig, -1, kx_end);
     }
   }
   if (do_y) {
-#pragma unroll 1
-    for (int seg = 0; seg < 3; ++seg) {
-      const int delta = seg == 0 ? 0 : (seg == 1 ? 1 : -1);
-      const double* tab = gens + (3 + seg) * C::GL + C::NP - tig;
-      const double* br = Vt + vt_idx<C>(tig, 16 * ucol + gq + delta);
-      int ra[C::WR], rb[C::WR];
-#pragma unroll
-      for (int mr = 0; mr < C::WR; ++mr) {
-        ra[mr] = prow<C>(urow + mr, gq);
-        rb[mr] = prow<C>(urow + mr, gq + 8);
-      }
-#pragma unroll 4
-      for (int l0 = 0; l0 < ky_end; l0 += 4) {
-        double a[C::WR][2], b[C::NF];
-#pragma unroll
-        for (int mr = 0; mr < C::WR; ++mr) {
-          a[mr][0] = tab[ra[mr] - l0];
-          a[mr][1] = tab[rb[mr] - l0];
-        }
-#pragma unroll
-        for (int nf = 0; nf < C::NF; ++nf) b[nf] = br[l0 * C::S + 8 * nf];
-#pragma unroll
-        for (int mr = 0; mr < C::WR; ++mr)
-#pragma unroll
-          for (int nf = 0; nf < C::NF; ++nf) dmma(acc[mr][nf], a[mr][0], a[mr][1], b[nf]);
-      }
+    const double* tab = gens + 3 * C::GL + C::NP - tig;
+    matvec_yseg<C, false>(Vt, tab, acc, urow, ucol, gq, tig, 0, ky_end);
+    if (merge & 2) {
+      matvec_yseg<C, true>(Vt, tab + C::GL, acc, urow, ucol, gq, tig, 1, ky_end);
+    } else {
+      matvec_yseg<C, false>(Vt, tab + C::GL, acc, urow, ucol, gq, tig, 1, ky_end);
+      matvec_yseg<C, false>(Vt, tab + 2 * C::GL, acc, urow, ucol, gq, tig, -1, ky_end);
     }
   }
 }

@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           load_vec<C>(Vt, W.d_src + (int64_t)(n - 1) * W.src_stride, nx, ny, c);
           __syncthreads();
         }
-        matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true);
+        matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true, P.merge);
       }
       int64_t nmv = need_in ? 1 : 0;
       int64_t npc = 0;  // preconditioner applications
@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
         __syncthreads();
         load_vec<C>(Vt, W.d_x0 + (int64_t)n * W.x0_stride, nx, ny, c);
         __syncthreads();
-        matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true);
+        matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true, P.merge);
         ++nmv;
         zero_part<C>(part[1]);
         RM_FOR_ELEM {
@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
         const double* Gr = W.d_gadd ? W.d_gadd + (int64_t)n * W.gadd_stride : nullptr;
         load_guess<C>(Vt, W.d_guess + (int64_t)n * W.guess_stride, Gr, nx, ny, c);
         __syncthreads();
-        matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true);
+        matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true, P.merge);
         ++nmv;
         double pg[1][C::WR][C::WC];
         zero_part<C>(pg[0]);
@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
         }
         RM_T(7);
         // Ap and p'Ap
-        matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true);
+        matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true, P.merge);
         ++nmv;
         RM_T(0);
         double p1[1][C::WR][C::WC];
@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
             if (j < ny && i < nx) Vt[vt_idx<C>(j, i)] = xs[elem_xidx<C>(c, mr, nf, e)];
           }
           bcast_band<C>(bc, c.rank, c.tid);
-          matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true);
+          matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true, P.merge);
           ++nmv;
           zero_part<C>(p1[0]);
           RM_FOR_ELEM {
@@ -664,7 +664,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) apply_kernel(const ApplyArgs P)
   const bool dox = P.which == 0 || P.which == 2;
   const bool doy = P.which == 0 || P.which == 3;
   if (dox || doy)
-    matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, (nx + 3) & ~3, (ny + 3) & ~3, dox, doy);
+    matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, (nx + 3) & ~3, (ny + 3) & ~3, dox, doy, P.merge);
   double sc = 0.0;
   if (P.which == 0) sc = P.sign * 0.5 * P.dt[b];
   if (P.which == 2) sc = 1.0 / P.kx;
@@ -706,6 +706,7 @@ __device__ __forceinline__ void lcg_jump(u128 mult, u128 plus, uint64_t delta, u
   ap = acc_p;
 }
 
+#ifndef RM_CASE_NP  // per-case translation units hold only their chain kernel instantiation
 __global__ void pcg64_kernel(PcgArgs P) {
   const u128 MULT = ((u128)0x2360ED051FC65DA4ull << 64) | (u128)0x4385DF649FCCF645ull;
   const u128 inc = ((u128)P.inc_hi << 64) | P.inc_lo;
@@ -759,12 +760,14 @@ __global__ void diff_sqnorm_kernel(int64_t n, const double* a, const double* b, 
   }
 }
 
+#endif
+
 // ----------------------------------------------------------------------------
 // launch helpers (instantiations)
 // ----------------------------------------------------------------------------
 
 template <int NP, int G>
-static cudaError_t launch_chain_t(const ChainArgs& a, int max_clusters, cudaStream_t st) {
+cudaError_t launch_chain_t(const ChainArgs& a, int max_clusters, cudaStream_t st) {
   using C = Cfg<NP, G>;
   auto kern = a.sw.precond ? chain_kernel<C, true> : chain_kernel<C, false>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
@@ -792,7 +795,7 @@ static cudaError_t launch_chain_t(const ChainArgs& a, int max_clusters, cudaStre
 }
 
 template <int NP, int G>
-static cudaError_t max_clusters_t(int* out) {
+cudaError_t max_clusters_t(int* out) {
   using C = Cfg<NP, G>;
   auto kern = chain_kernel<C, true>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
@@ -826,6 +829,17 @@ static cudaError_t max_clusters_t(int* out) {
   X(128, 4)               \
   X(128, 8)               \
   X(128, 16)
+
+#ifdef RM_CASE_NP
+// build.py compiles this file once per (NP, G) case with -DRM_CASE_NP/-DRM_CASE_G (parallel nvcc jobs)
+template cudaError_t launch_chain_t<RM_CASE_NP, RM_CASE_G>(const ChainArgs&, int, cudaStream_t);
+template cudaError_t max_clusters_t<RM_CASE_NP, RM_CASE_G>(int*);
+#else
+#define X(A, B)                                                                              \
+  extern template cudaError_t launch_chain_t<A, B>(const ChainArgs&, int, cudaStream_t); \
+  extern template cudaError_t max_clusters_t<A, B>(int*);
+RM_CHAIN_CASES(X)
+#undef X
 
 bool chain_supported(int np, int g) {
 #define X(a, b) \
@@ -902,5 +916,7 @@ cudaError_t launch_diff_sqnorm(int64_t n, const double* a, const double* b, doub
   diff_sqnorm_kernel<<<1, 1024, 0, st>>>(n, a, b, out);
   return cudaGetLastError();
 }
+
+#endif  // RM_CASE_NP
 
 }  // namespace rm

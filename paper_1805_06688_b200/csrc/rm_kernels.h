@@ -14,6 +14,7 @@ struct ChainArgs {
   int nx, ny;
   double cm;
   const double* gens;  // 6 generator tables of length 2*NP+8 (device)
+  int merge;           // bit 0/1: merged off-diagonal x/y segments (see matvec)
   double* scratch;     // NP*NP doubles per cluster (device): right-hand side b
   int* chain_counter;  // work counter, zeroed before launch
   int* fail;           // first-failure flag
@@ -29,6 +30,7 @@ struct ApplyArgs {
   int nx, ny, which, sign;
   double cm, kx, ky;
   const double* gens;
+  int merge;
   const double* dt;
   const double* v;
   int64_t v_stride;

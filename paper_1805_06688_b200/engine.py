@@ -98,6 +98,7 @@ class Engine:
         _native.check(self.lib.rm_grid_create(self.nx, self.ny, *ptrs, gens.sx, gens.sy, self.kx, self.ky,
                                               gens.mass_scale, C.byref(handle)), "rm_grid_create")
         self.handle = handle
+        self.flags = int(self.lib.rm_grid_flags(handle))  # bit 0/1: merged off-diagonal x/y matvec segments
         self.launches = 0
         self.trace = None  # list of (tag, start event, end event, counters-before) when profiling
 

@@ -1,0 +1,23 @@
+"""Algorithmic FLOP counts of the hot path's two kernels-within-the-kernel.
+
+Used by bench.py (roofline "achieved") and tools/profile_solve.py.  Counts are the arithmetic the
+algorithm as implemented needs, not what the tensor cores execute on zero padding.
+"""
+
+from __future__ import annotations
+
+
+def fmv(nx: int, ny: int, merge: int = 0) -> float:
+    """One combined-operator apply (M + s K) v: per direction a diagonal-block Toeplitz product
+    along every row, plus the two off-diagonal ones (rows j+-1) -- or, when the off-diagonal block is
+    shifted-symmetric (``merge`` bit, rm_grid_flags), one length-(n+1) product of the pre-added
+    neighbours -- then the 7-point mass stencil and the combination (13 per DOF)."""
+    fx = 2.0 * nx * nx * ny + (2.0 * nx * (nx + 1) * ny + nx * ny if merge & 1 else 2.0 * nx * nx * 2 * (ny - 1))
+    fy = 2.0 * ny * ny * nx + (2.0 * ny * (ny + 1) * nx + nx * ny if merge & 2 else 2.0 * ny * ny * 2 * (nx - 1))
+    return fx + fy + 13.0 * nx * ny
+
+
+def fpc(nx: int, ny: int) -> float:
+    """One tau-preconditioner application: two even/odd-folded DST-I contractions per direction
+    (half the dense count), the folds and the diagonal scaling."""
+    return 2.0 * nx * ny * (nx + ny) + 5.0 * nx * ny

@@ -15,17 +15,10 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 from paper_1805_06688_b200.configs import make_case  # noqa: E402
+from paper_1805_06688_b200.flops import fmv, fpc  # noqa: E402
 from paper_1805_06688_b200.engine import Engine  # noqa: E402
 from paper_1805_06688_b200.mgrit import MgritOptions, solve  # noqa: E402
 from paper_1805_06688_b200.stepper import ProblemSpec  # noqa: E402
-
-
-def fmv(nx, ny):
-    return 2 * nx * nx * (3 * ny - 2) + 2 * ny * ny * (3 * nx - 2) + 13 * nx * ny
-
-
-def fpc(nx, ny):
-    return 2 * nx * ny * (nx + ny) + 5 * nx * ny
 
 
 def main():
@@ -45,7 +38,7 @@ def main():
     opts = MgritOptions(m=case.m, max_levels=lv, halt_tol=case.halt_tol, cg_rel_tol=case.cg_rel_tol,
                         cg_preconditioner=a.precond)
     eng = Engine.for_problem(case.grid, case.beta, case.gamma, case.kx, case.ky)
-    F = fmv(case.grid.nx, case.grid.ny)
+    F = fmv(case.grid.nx, case.grid.ny, eng.flags)
     FP = fpc(case.grid.nx, case.grid.ny)
     for rep in range(a.repeat):
         eng.start_trace()
