@@ -208,10 +208,12 @@ __device__ __forceinline__ void matvec(const double* __restrict__ Vt, const doub
 // u_b = v_b + v_{NP-2-b} (b < HALF-1), u_{HALF-1} = v_{HALF-1}, w_b = v_b - v_{NP-2-b}:
 //   outputs a even (alpha = a+1 odd):  sum_{b<HALF} S[a][b] u_b
 //   outputs a odd  (alpha even):       sum_{b<HALF-1} S[a][b] w_b
-// The folded vector is stored in place as u at [0, HALF) and w at [HALF, NP-1) (entry NP-1 is the
-// zero padding): half the contraction length.  fold_rows/fold_cols do it for a tile.
+// The fold is applied on the fly to the B operand of the contraction (b = v_b +- v_{NP-2-b}, one
+// FMA with a +-1 multiplier: bitwise the same sums as an explicit fold), so the tile is never
+// modified in place and no barrier is needed between the exchange and the contraction.  With the
+// natural layout, b = HALF-1 pairs with itself: its multiplier is 0 for u (u = v) and -1 for w (0).
 
-// y-direction DST, normal mapping: out[j][i] = sum_l Sy[j][l] V[l][i]  (V folded along rows if fold)
+// y-direction DST, normal mapping: out[j][i] = sum_l Sy[j][l] V[l][i]  (folded along rows if fold)
 template <class C>
 __device__ __forceinline__ void dst_y(const double* __restrict__ Vt, const double* __restrict__ tab, int L,
                                       double (&acc)[C::WR][C::NF][4], int urow, int ucol, int gq, int tig,
@@ -224,11 +226,30 @@ __device__ __forceinline__ void dst_y(const double* __restrict__ Vt, const doubl
   const int ja = prow<C>(urow, gq) + 1, jb = prow<C>(urow, gq + 8) + 1;  // alpha = j + 1
   int ia = (ja * (tig + 1)) % L, ib = (jb * (tig + 1)) % L;
   const int sa = (4 * ja) % L, sb = (4 * jb) % L;
-  const int rowoff = (fold && (urow & 1)) ? C::HALF : 0;  // odd unit rows: alpha even -> w half
-  const int kend = fold ? C::HALF : k_end;
-  const double* br = Vt + vt_idx<C>(tig + rowoff, 16 * ucol + gq);
+  const double* br = Vt + vt_idx<C>(tig, 16 * ucol + gq);
+  if (fold) {
+    // odd unit rows hold alpha even -> w (difference); even unit rows -> u (sum)
+    const double sgn = (urow & 1) ? -1.0 : 1.0;
+    const double sgn_last = (tig == 3) ? ((urow & 1) ? -1.0 : 0.0) : sgn;
+    const double* bp = br + (C::NP - 2 - 2 * tig) * C::S;  // row NP-2-l for row l = l0 + tig
 #pragma unroll 4
-  for (int l0 = 0; l0 < kend; l0 += 4) {
+    for (int l0 = 0; l0 < C::HALF; l0 += 4) {
+      const double a0 = tab[ia], a1 = tab[ib];
+      const double f = l0 == C::HALF - 4 ? sgn_last : sgn;
+      double b[C::NF];
+#pragma unroll
+      for (int nf = 0; nf < C::NF; ++nf) b[nf] = fma(f, bp[8 * nf - l0 * C::S], br[l0 * C::S + 8 * nf]);
+#pragma unroll
+      for (int nf = 0; nf < C::NF; ++nf) dmma(acc[0][nf], a0, a1, b[nf]);
+      ia += sa;
+      ia -= ia >= L ? L : 0;
+      ib += sb;
+      ib -= ib >= L ? L : 0;
+    }
+    return;
+  }
+#pragma unroll 4
+  for (int l0 = 0; l0 < k_end; l0 += 4) {
     const double a0 = tab[ia], a1 = tab[ib];
     double b[C::NF];
 #pragma unroll
@@ -250,7 +271,7 @@ __device__ __forceinline__ int fold_alpha(int m, bool fold) {
 }
 
 // x-direction DST, transposed mapping: out^T[i][j] = sum_k Sx[i][k] V[j][k], j over the rows of
-// units tn .. tn+WC-1 (V folded along columns if fold)
+// units tn .. tn+WC-1 (folded along columns if fold: m-tiles below HALF -> u, above -> w)
 template <class C>
 __device__ __forceinline__ void dst_xT(const double* __restrict__ Vt, const double* __restrict__ tab, int L,
                                        double (&acc)[C::WR][C::NF][4], int tm, int tn, int gq, int tig,
@@ -262,13 +283,32 @@ __device__ __forceinline__ void dst_xT(const double* __restrict__ Vt, const doub
   const int xa = fold_alpha<C>(16 * tm + gq, fold), xb = fold_alpha<C>(16 * tm + gq + 8, fold);
   int ia = (xa * (tig + 1)) % L, ib = (xb * (tig + 1)) % L;
   const int sa = (4 * xa) % L, sb = (4 * xb) % L;
-  const int coloff = (fold && 16 * tm >= C::HALF) ? C::HALF : 0;
-  const int kend = fold ? C::HALF : k_end;
   const double* br[C::NF];
 #pragma unroll
-  for (int nf = 0; nf < C::NF; ++nf) br[nf] = Vt + vt_idx<C>(prow<C>(tn + (nf >> 1), 8 * (nf & 1) + gq), tig + coloff);
+  for (int nf = 0; nf < C::NF; ++nf) br[nf] = Vt + vt_idx<C>(prow<C>(tn + (nf >> 1), 8 * (nf & 1) + gq), tig);
+  if (fold) {
+    const bool w = 16 * tm >= C::HALF;
+    const double sgn = w ? -1.0 : 1.0;
+    const double sgn_last = (tig == 3) ? (w ? -1.0 : 0.0) : sgn;
+    const int off = C::NP - 2 - 2 * tig;  // column NP-2-k for column k = k0 + tig
 #pragma unroll 4
-  for (int k0 = 0; k0 < kend; k0 += 4) {
+    for (int k0 = 0; k0 < C::HALF; k0 += 4) {
+      const double a0 = tab[ia], a1 = tab[ib];
+      const double f = k0 == C::HALF - 4 ? sgn_last : sgn;
+      double b[C::NF];
+#pragma unroll
+      for (int nf = 0; nf < C::NF; ++nf) b[nf] = fma(f, br[nf][off - k0], br[nf][k0]);
+#pragma unroll
+      for (int nf = 0; nf < C::NF; ++nf) dmma(acc[0][nf], a0, a1, b[nf]);
+      ia += sa;
+      ia -= ia >= L ? L : 0;
+      ib += sb;
+      ib -= ib >= L ? L : 0;
+    }
+    return;
+  }
+#pragma unroll 4
+  for (int k0 = 0; k0 < k_end; k0 += 4) {
     const double a0 = tab[ia], a1 = tab[ib];
     double b[C::NF];
 #pragma unroll
@@ -279,45 +319,6 @@ __device__ __forceinline__ void dst_xT(const double* __restrict__ Vt, const doub
     ia -= ia >= L ? L : 0;
     ib += sb;
     ib -= ib >= L ? L : 0;
-  }
-}
-
-// fold the columns of rows {prow(ur, t)} for unit rows [ur0, ur0+nur) (in place, see above)
-template <class C>
-__device__ __forceinline__ void fold_cols(double* Vt, int ur0, int nur, int tid) {
-  constexpr int H = C::HALF, NT = H / 2;  // pair tasks (c, H-2-c) per row
-  const int ntask = nur * 16 * NT;
-  for (int t = tid; t < ntask; t += C::THREADS) {
-    const int rr = t / NT, cc = t % NT;
-    double* row = Vt + vt_idx<C>(prow<C>(ur0 + rr / 16, rr % 16), 0);
-    const int c1 = cc, c2 = H - 2 - cc;
-    const double a1 = row[c1], b1 = row[C::NP - 2 - c1], a2 = row[c2], b2 = row[C::NP - 2 - c2];
-    row[c1] = a1 + b1;
-    row[H + c1] = a1 - b1;
-    if (c2 != c1) {
-      row[c2] = a2 + b2;
-      row[H + c2] = a2 - b2;
-    }
-  }
-}
-
-// fold the rows of the whole tile (all columns, in place)
-template <class C>
-__device__ __forceinline__ void fold_rows(double* Vt, int tid) {
-  constexpr int H = C::HALF, NT = H / 2;
-  const int ntask = C::NP * NT;
-  for (int t = tid; t < ntask; t += C::THREADS) {
-    const int i = t % C::NP, cc = t / C::NP;
-    const int c1 = cc, c2 = H - 2 - cc;
-    double* col = Vt + vt_idx<C>(0, i);
-    const double a1 = col[c1 * C::S], b1 = col[(C::NP - 2 - c1) * C::S];
-    const double a2 = col[c2 * C::S], b2 = col[(C::NP - 2 - c2) * C::S];
-    col[c1 * C::S] = a1 + b1;
-    col[(H + c1) * C::S] = a1 - b1;
-    if (c2 != c1) {
-      col[c2 * C::S] = a2 + b2;
-      col[(H + c2) * C::S] = a2 - b2;
-    }
   }
 }
 

@@ -23,6 +23,7 @@ namespace rm {
 #ifdef RM_TIMING
 // phase timing of CTA 0 (debug builds only: python -m paper_1805_06688_b200.build --timing)
 #define RM_T0() long long t_mark_ = clock64();
+#define RM_TM() t_mark_ = clock64()
 #define RM_T(slot)                                                     \
   do {                                                                 \
     long long t_now_ = clock64();                                      \
@@ -31,6 +32,7 @@ namespace rm {
   } while (0)
 #else
 #define RM_T0()
+#define RM_TM()
 #define RM_T(slot)
 #endif
 
@@ -43,7 +45,6 @@ struct Ctx {
   int tid, lane, warp, gq, tig, rank;
   int urow, ucol;  // first unit (row, col) of this warp
   int tm, tn;      // transposed DST stage: unit column (m) and first unit row (n) of this warp
-  int own_ur0, own_nur;  // unit rows owned by this CTA (x-fold of the DST)
   int tm_fold;           // transposed-stage m unit when the x-direction DST is folded
 };
 
@@ -121,10 +122,12 @@ struct Smem {
 
 // z = P^{-1} r for the tau preconditioner: T1 = R Sx; T2 = Sy T1 * dinv; T3 = T2 Sx; z = Sy T3.
 // The x-direction stages read only this CTA's own rows (transposed mapping), so their inputs are
-// written locally without any exchange; only the y-stage inputs (T1, T3) are broadcast.  A cluster
-// barrier after each broadcast guarantees every outgoing bulk copy has landed before the own band is
-// folded in place.  Precondition: every CTA finished reading its operand tile and nobody reads this
-// CTA's own rows any more.  Result z in acc (normal mapping).
+// written locally without any exchange; only the y-stage inputs (T1, T3) are broadcast.  The DST
+// folds are applied on the fly (rm_device.cuh), so the tile is never modified in place: the only
+// cluster barrier inside is the one between the passes (every peer has received this CTA's band and
+// finished its y-stage before the own rows are overwritten and new bands are pushed).
+// Precondition: every CTA finished reading its operand tile and nobody reads this CTA's own rows any
+// more.  Result z in acc (normal mapping).
 template <class C>
 __device__ __forceinline__ void apply_tau(const Ctx<C>& c, const Smem<C>& sm, Bcast<C>& bc,
                                           const double (&r)[C::WR][C::NF][4], double (&acc)[C::WR][C::NF][4],
@@ -153,29 +156,21 @@ __device__ __forceinline__ void apply_tau(const Ctx<C>& c, const Smem<C>& sm, Bc
 #pragma unroll 1
   for (int pass = 0; pass < 2; ++pass) {
     if constexpr (C::G > C::UR) {
-      // two CTAs share each own row (column halves): exchange the halves, and let every outgoing
-      // copy land before the rows are folded in place
+      // two CTAs share each own row (column halves): exchange the halves
       bcast_band<C>(bc, c.rank, c.tid);
-      group_sync<C::G>();
     }
     // x-direction (transposed mapping) on the CTA's own rows
-    if (fold_x) {
-      fold_cols<C>(Vt, c.own_ur0, c.own_nur, c.tid);
-      __syncthreads();
-    }
     dst_xT<C>(Vt, sm.tabx, Lx, acc, tm, c.tn, c.gq, c.tig, kx_end, fold_x);
-    __syncthreads();
+    if constexpr (C::G > C::UR)
+      group_sync<C::G>();  // the row-sharing peer received our half and finished reading its copy
+    else
+      __syncthreads();
     RM_T(9);
     RM_FOR_ELEM {
       const int j = elemT_row<C>(c, nf, e), i = fold_alpha<C>(16 * tm + c.gq + 8 * (e >> 1), fold_x) - 1;
       if (j < ny && i < nx) Vt[vt_idx<C>(j, i)] = acc[mr][nf][e];
     }
     bcast_band<C>(bc, c.rank, c.tid);
-    if (fold_y) {
-      if constexpr (C::G > 1) group_sync<C::G>();  // all outgoing copies of the own band completed
-      fold_rows<C>(Vt, c.tid);
-      __syncthreads();
-    }
     RM_T(10);
     // y-direction (normal mapping) over all rows
     dst_y<C>(Vt, sm.taby, Ly, acc, c.urow, c.ucol, c.gq, c.tig, ky_end, fold_y);
@@ -234,8 +229,6 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
     constexpr int tcols = C::CR / C::WC > 0 ? C::CR / C::WC : 1;
     c.tm = c0 + c.warp / tcols;
     c.tn = r0 + (c.warp % tcols) * C::WC;
-    c.own_ur0 = r0;
-    c.own_nur = C::CR;
     c.tm_fold = c.tm;
     if constexpr (C::G > C::UR) {
       // two CTAs share a unit row (column halves): with the fold, output column i = alpha - 1 comes
@@ -489,7 +482,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           // z = P^-1 r; reduce r.r (convergence test) and r.z together
           apply_tau<C>(c, sm, bc, rr_, acc, dinv, nx, ny, Lx, Ly, P.timing);
           ++npc;
-          RM_T0();
+          RM_TM();
           RM_FOR_ELEM { part2[1][mr][nf >> 1] += rr_[mr][nf][e] * acc[mr][nf][e]; }
           group_reduce<C, 2>(part2, red, sm.red_peer, buf, c.urow, c.ucol, c.lane, red2);
         } else {

@@ -9,6 +9,7 @@ without the shared library, raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -16,6 +17,8 @@ import torch
 
 from . import _native
 from .krylov import CgFailure
+
+_NVTX = os.environ.get("RM_NVTX") == "1"  # name every sweep launch for ncu --nvtx-include
 
 __all__ = ["Engine", "require_cuda", "generators_for"]
 
@@ -190,7 +193,11 @@ class Engine:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             before = counters.clone()
             e0.record()
+        if _NVTX:
+            torch.cuda.nvtx.range_push(tag or "sweep")
         _native.check(self.lib.rm_sweep_run(self.handle, C.byref(sw), _stream()), "rm_sweep_run")
+        if _NVTX:
+            torch.cuda.nvtx.range_pop()
         self.launches += 1
         if self.trace is not None:
             e1.record()
