@@ -358,7 +358,6 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
   const int64_t max_iter = W.max_iter > 0 ? W.max_iter : 10 * (int64_t)ndof;
   const bool need_in = W.explicit_rhs || W.x0_mode == 1;
 
-  for (int i = c.tid; i < 6 * C::GL; i += C::THREADS) gens[i] = P.gens[i];
   if constexpr (PRE) {
     for (int i = c.tid; i < Lx; i += C::THREADS) tabx[i] = P.tabx[i];
     for (int i = c.tid; i < Ly; i += C::THREADS) taby[i] = P.taby[i];
@@ -405,6 +404,9 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
       int64_t nmv = need_in ? 1 : 0, npc = 0;
 
       if (need_in) {
+        // step-operator tables M - s K (rm_device.cuh build_step_tables); the previous step ended
+        // with a group barrier
+        build_step_tables<C::NP, C::GL, C::THREADS>(gens, P.gens, -s, cm, c.tid);
         if (!in_tile) {
           const double* src = W.d_src + (int64_t)(n - 1) * W.src_stride;
           RM_BIG_FOR {
@@ -412,6 +414,8 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
             if (j < ny && i < nx) put_tile(pv0, j, i, __ldcg(src + j * nx + i));
           }
           group_sync<C::G>();
+        } else {
+          __syncthreads();
         }
         big_matvec<C>(pv0, gens, stage, acc, c, kx_end, ky_end, P.merge);
       }
@@ -421,19 +425,15 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
         const int fi = big_fidx(c, nf, e);
         double b = 0.0, x = 0.0, r = 0.0;
         if (j < ny && i < nx) {
-          double mv = 0.0, kv = 0.0;
-          if (need_in) {
-            mv = big_mass<C>(pv0, j, i, cm);
-            kv = acc[nf][e];
-          }
-          if (W.explicit_rhs) b = mv + (-s) * kv;
+          const double am = need_in ? acc[nf][e] : 0.0;  // (M - s K) v
+          if (W.explicit_rhs) b = am;
           if (Fn) {
             const double f = fs * __ldcg(Fn + j * nx + i);
             b = W.explicit_rhs ? f + b : f;
           }
           if (W.x0_mode == 1) {
             x = __ldcg(pv0 + pv_idx<C>(j, i));
-            r = b - (mv + s * kv);
+            r = b - (2.0 * big_mass<C>(pv0, j, i, cm) - am);  // (M + s K) v = 2 M v - (M - s K) v
           } else {
             r = b;
           }
@@ -445,6 +445,9 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
         part[0][nf >> 1] += b * b;
         part[1][nf >> 1] += r * r;
       }
+      __syncthreads();
+      build_step_tables<C::NP, C::GL, C::THREADS>(gens, P.gens, s, cm, c.tid);  // M + s K from here on
+      __syncthreads();
       if (W.x0_mode == 2) {
         group_sync<C::G>();
         const double* x0 = W.d_x0 + (int64_t)n * W.x0_stride;
@@ -462,7 +465,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
           double x = 0.0, r = 0.0;
           if (j < ny && i < nx) {
             x = __ldcg(pv0 + pv_idx<C>(j, i));
-            r = bs[fi] - (big_mass<C>(pv0, j, i, cm) + s * acc[nf][e]);
+            r = bs[fi] - acc[nf][e];
           }
           xs[fi] = x;
           rs[fi] = r;
@@ -491,7 +494,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
         RM_BIG_FOR {
           const int j = big_row(c, e), i = big_col(c, nf, e);
           double r = 0.0;
-          if (j < ny && i < nx) r = bs[big_fidx(c, nf, e)] - (big_mass<C>(pv0, j, i, cm) + s * acc[nf][e]);
+          if (j < ny && i < nx) r = bs[big_fidx(c, nf, e)] - acc[nf][e];
           acc[nf][e] = r;
           pg[0][nf >> 1] += r * r;
         }
@@ -578,7 +581,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
           const int j = big_row(c, e), i = big_col(c, nf, e);
           double ap = 0.0;
           if (j < ny && i < nx) {
-            ap = big_mass<C>(pv0, j, i, cm) + s * acc[nf][e];
+            ap = acc[nf][e];
             p1[0][nf >> 1] += __ldcg(pv0 + pv_idx<C>(j, i)) * ap;
           }
           acc[nf][e] = ap;
@@ -652,7 +655,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
           RM_BIG_FOR {
             const int j = big_row(c, e), i = big_col(c, nf, e);
             double rt = 0.0;
-            if (j < ny && i < nx) rt = bs[big_fidx(c, nf, e)] - (big_mass<C>(pv0, j, i, cm) + s * acc[nf][e]);
+            if (j < ny && i < nx) rt = bs[big_fidx(c, nf, e)] - acc[nf][e];
             acc[nf][e] = rt;
             pt[0][nf >> 1] += rt * rt;
           }

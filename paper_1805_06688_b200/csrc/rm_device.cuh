@@ -322,6 +322,25 @@ __device__ __forceinline__ void dst_xT(const double* __restrict__ Vt, const doub
   }
 }
 
+// Step-operator tables: gs = s * base + cm * (P1 mass blocks), so that one contraction gives
+// (M + s K) v directly (the 7-point mass stencil is a block-Toeplitz operator with the same block
+// structure: x diagonal block tridiag(1, 6, 1), off-diagonal blocks with entries at d = 0, -1
+// (rows j+1) and d = 0, +1 (rows j-1), assembly.py:172-187).  The off-diagonal mass block is
+// shifted-symmetric too, so the merged segment stays valid.  Entries at |d| >= n only ever meet
+// zero padding.
+template <int NP, int GL, int THREADS>
+__device__ __forceinline__ void build_step_tables(double* __restrict__ gs, const double* __restrict__ base,
+                                                  double s, double cm, int tid) {
+  for (int idx = tid; idx < 6 * GL; idx += THREADS) {
+    const int t = idx / GL, d = idx - t * GL - NP;
+    double m = 0.0;
+    if (t == 0) m = d == 0 ? 6.0 : (d == 1 || d == -1) ? 1.0 : 0.0;
+    if (t == 1) m = (d == 0 || d == -1) ? 1.0 : 0.0;
+    if (t == 2) m = (d == 0 || d == 1) ? 1.0 : 0.0;
+    gs[idx] = fma(s, __ldg(base + idx), cm * m);
+  }
+}
+
 // cm * (6 V(j,i) + V(j,i-1) + V(j,i+1) + V(j+1,i) + V(j+1,i+1) + V(j-1,i) + V(j-1,i-1))
 // (mass_generators, assembly.py:172-187, applied as a 7-point stencil).
 template <class C>

@@ -261,7 +261,6 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
   const bool need_in = W.explicit_rhs || W.x0_mode == 1;
 
   for (int i = c.tid; i < C::VT; i += C::THREADS) Vt[i] = 0.0;
-  for (int i = c.tid; i < 6 * C::GL; i += C::THREADS) gens[i] = P.gens[i];
   if constexpr (PRE) {
     for (int i = c.tid; i < Lx; i += C::THREADS) sm.tabx[i] = P.tabx[i];
     for (int i = c.tid; i < Ly; i += C::THREADS) sm.taby[i] = P.taby[i];
@@ -299,11 +298,11 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
       const double* Fn = W.d_f ? W.d_f + (int64_t)n * W.f_stride : nullptr;
 
       // ---------------- right-hand side, initial iterate and residual --------------
+      // (the previous step ended with a group barrier: nobody reads the tables any more)
       if (need_in) {
-        if (!in_tile) {
-          load_vec<C>(Vt, W.d_src + (int64_t)(n - 1) * W.src_stride, nx, ny, c);
-          __syncthreads();
-        }
+        build_step_tables<C::NP, C::GL, C::THREADS>(gens, P.gens, -s, cm, c.tid);  // M - s K
+        if (!in_tile) load_vec<C>(Vt, W.d_src + (int64_t)(n - 1) * W.src_stride, nx, ny, c);
+        __syncthreads();
         matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true, P.merge);
       }
       int64_t nmv = need_in ? 1 : 0;
@@ -316,19 +315,16 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
         double b = 0.0, x = 0.0, r = 0.0;
         const int si = elem_sidx<C>(c, mr, nf, e);
         if (j < ny && i < nx) {
-          double mv = 0.0, kv = 0.0;
-          if (need_in) {
-            mv = mass_stencil<C>(Vt, j, i, cm);
-            kv = acc[mr][nf][e];
-          }
-          if (W.explicit_rhs) b = mv + (-s) * kv;
+          const double am = need_in ? acc[mr][nf][e] : 0.0;  // (M - s K) v
+          if (W.explicit_rhs) b = am;
           if (Fn) {
             const double f = fs * __ldcg(Fn + j * nx + i);
             b = W.explicit_rhs ? f + b : f;
           }
           if (W.x0_mode == 1) {
+            // x0 = v: (M + s K) v = 2 M v - (M - s K) v
             x = Vt[vt_idx<C>(j, i)];
-            r = b - (mv + s * kv);
+            r = b - (2.0 * mass_stencil<C>(Vt, j, i, cm) - am);
           } else {
             r = b;  // x0 = 0: r = b - A*0 (krylov.py:47,50)
           }
@@ -340,9 +336,11 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
         part[0][mr][nf >> 1] += b * b;
         part[1][mr][nf >> 1] += r * r;
       }
+      __syncthreads();
+      build_step_tables<C::NP, C::GL, C::THREADS>(gens, P.gens, s, cm, c.tid);  // M + s K from here on
+      __syncthreads();
       if (W.x0_mode == 2) {
         // given initial iterate (spacetime_residual, stepper.py:203)
-        __syncthreads();
         load_vec<C>(Vt, W.d_x0 + (int64_t)n * W.x0_stride, nx, ny, c);
         __syncthreads();
         matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true, P.merge);
@@ -353,7 +351,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           double x = 0.0, r = 0.0;
           if (j < ny && i < nx) {
             x = Vt[vt_idx<C>(j, i)];
-            r = sb_[elem_sidx<C>(c, mr, nf, e)] - (mass_stencil<C>(Vt, j, i, cm) + s * acc[mr][nf][e]);
+            r = sb_[elem_sidx<C>(c, mr, nf, e)] - acc[mr][nf][e];
           }
           xs[elem_xidx<C>(c, mr, nf, e)] = x;
           rr_[mr][nf][e] = r;
@@ -379,7 +377,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
           double r = 0.0;
           if (j < ny && i < nx)
-            r = sb_[elem_sidx<C>(c, mr, nf, e)] - (mass_stencil<C>(Vt, j, i, cm) + s * acc[mr][nf][e]);
+            r = sb_[elem_sidx<C>(c, mr, nf, e)] - acc[mr][nf][e];
           acc[mr][nf][e] = r;
           pg[0][mr][nf >> 1] += r * r;
         }
@@ -444,7 +442,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
           double ap = 0.0;
           if (j < ny && i < nx) {
-            ap = mass_stencil<C>(Vt, j, i, cm) + s * acc[mr][nf][e];
+            ap = acc[mr][nf][e];
             p1[0][mr][nf >> 1] += Vt[vt_idx<C>(j, i)] * ap;
           }
           acc[mr][nf][e] = ap;
@@ -519,7 +517,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
             const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
             double rt = 0.0;
             if (j < ny && i < nx)
-              rt = sb_[elem_sidx<C>(c, mr, nf, e)] - (mass_stencil<C>(Vt, j, i, cm) + s * acc[mr][nf][e]);
+              rt = sb_[elem_sidx<C>(c, mr, nf, e)] - acc[mr][nf][e];
             acc[mr][nf][e] = rt;
             p1[0][mr][nf >> 1] += rt * rt;
           }

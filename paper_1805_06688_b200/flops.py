@@ -11,10 +11,11 @@ def fmv(nx: int, ny: int, merge: int = 0) -> float:
     """One combined-operator apply (M + s K) v: per direction a diagonal-block Toeplitz product
     along every row, plus the two off-diagonal ones (rows j+-1) -- or, when the off-diagonal block is
     shifted-symmetric (``merge`` bit, rm_grid_flags), one length-(n+1) product of the pre-added
-    neighbours -- then the 7-point mass stencil and the combination (13 per DOF)."""
+    neighbours.  The P1 mass and the step scale s are folded into the Toeplitz tables once per step
+    (rm_device.cuh build_step_tables), so they add no per-apply arithmetic."""
     fx = 2.0 * nx * nx * ny + (2.0 * nx * (nx + 1) * ny + nx * ny if merge & 1 else 2.0 * nx * nx * 2 * (ny - 1))
     fy = 2.0 * ny * ny * nx + (2.0 * ny * (ny + 1) * nx + nx * ny if merge & 2 else 2.0 * ny * ny * 2 * (nx - 1))
-    return fx + fy + 13.0 * nx * ny
+    return fx + fy
 
 
 def fpc(nx: int, ny: int) -> float:
