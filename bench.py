@@ -275,7 +275,6 @@ def run_ours(args):
         _, tr = solve(spec, opts, device_result=True, engine=eng)
         iters = tr.iterations
     barrier()
-    eng.start_trace()
     launches0 = eng.launches
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
@@ -285,9 +284,14 @@ def run_ours(args):
             U, tr = solve(spec, opts, device_result=True, engine=eng)
         e1.record()
         barrier()
-    trace = eng.stop_trace()
     launches = eng.launches - launches0
     ms = e0.elapsed_time(e1) / args.steps
+    # one more (untimed) solve with per-launch CUDA events and counter snapshots: the chain kernel's
+    # share of the step and its algorithmic FLOPs (roofline)
+    eng.start_trace()
+    solve(spec, opts, device_result=True, engine=eng)
+    barrier()
+    trace = eng.stop_trace()
     if dist is not None:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -303,8 +307,13 @@ def run_ours(args):
     traffic, traffic_launch = ncu_traffic()
 
     # end to end through the public API (host inputs, host result)
+    # (one untimed call first: the public API's engine cache and the page-locked result block are
+    # built once per process; each result is released before the next call, as a caller looping over
+    # solves would)
     e2e_ms = []
+    Uh, tr_h = solve(spec, opts)
     for _ in range(args.steps):
+        Uh = None
         barrier()
         t0 = time.perf_counter()
         Uh, tr_h = solve(spec, opts)
@@ -343,10 +352,10 @@ def run_ours(args):
                          "kernel": "chain_kernel (FP64 DMMA block-Toeplitz matvec + fused CG)",
                          "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (FP64 not in MEASURED_PEAKS.json)",
                          "traffic_launch": traffic_launch,
-                         "flops_per_apply": fmv(case.grid.nx, case.grid.ny, eng.flags), "applies_per_step": mvs // args.steps,
+                         "flops_per_apply": fmv(case.grid.nx, case.grid.ny, eng.flags), "applies_per_step": mvs,
                          "flops_per_precond": fpc(case.grid.nx, case.grid.ny),
-                         "precond_applies_per_step": pcs // args.steps,
-                         "kernel_ms_per_step": k_ms / args.steps},
+                         "precond_applies_per_step": pcs,
+                         "kernel_ms_per_step": k_ms},
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,
         }

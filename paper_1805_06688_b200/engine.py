@@ -29,6 +29,16 @@ _CG_MESSAGES = {
 }
 
 
+def to_host(t: torch.Tensor) -> np.ndarray:
+    """Device tensor -> numpy through page-locked memory (torch's caching host allocator: repeated
+    results of the same size reuse the pinned block once the previous array is released)."""
+    if t.device.type != "cuda":
+        return t.numpy()
+    host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    host.copy_(t)
+    return host.numpy()
+
+
 def require_cuda() -> torch.device:
     if not torch.cuda.is_available():
         raise RuntimeError("riesz_mgrit_b200 needs a CUDA device (B200, sm_100a); no CPU fallback exists")
@@ -115,6 +125,21 @@ class Engine:
     @classmethod
     def for_problem(cls, grid, beta, gamma, kx, ky) -> "Engine":
         return cls(grid.nx, grid.ny, generators_for(grid, beta, gamma), kx, ky)
+
+    _cache: dict = {}
+
+    @classmethod
+    def shared(cls, grid, beta, gamma, kx, ky) -> "Engine":
+        """A process-wide engine per (grid, coefficients, device), reused by repeated public-API calls
+        (the device context, generator tables and tau diagonals are built once)."""
+        key = (grid.nx, grid.ny, float(grid.hx), float(grid.hy), float(beta), float(gamma), float(kx), float(ky),
+               torch.cuda.current_device() if torch.cuda.is_available() else -1)
+        eng = cls._cache.get(key)
+        if eng is None:
+            if len(cls._cache) >= 2:
+                cls._cache.pop(next(iter(cls._cache)))
+            eng = cls._cache[key] = cls.for_problem(grid, beta, gamma, kx, ky)
+        return eng
 
     def ensure_tau(self) -> None:
         """Install the tau preconditioner (host O(n^3) setup, once per grid; precond.py)."""

@@ -17,7 +17,7 @@ import torch
 
 from . import assembly
 from .assembly import device_implicit_solve, from_device, to_device_2d
-from .engine import Engine, gauss_tau, require_cuda
+from .engine import Engine, gauss_tau, require_cuda, to_host
 from .krylov import CgOptions
 from .loads import HatQuadrature
 from .mesh import SpatialGrid, TemporalMesh
@@ -94,7 +94,7 @@ class Discretization:
         self._tq = np.polynomial.legendre.leggauss(time_quad_points)
         self.time_quad_points = time_quad_points
         self.device = require_cuda()
-        self.engine = engine or Engine.for_problem(grid, spec.beta, spec.gamma, spec.kx, spec.ky)
+        self.engine = engine or Engine.shared(grid, spec.beta, spec.gamma, spec.kx, spec.ky)
         self.counters = torch.zeros(4, dtype=torch.int64, device=self.device)
         self._combined: dict = {}
         self._mg = None
@@ -233,7 +233,7 @@ def sequential_solve(spec: ProblemSpec, disc: Discretization | None = None, *, d
         disc.engine.check_fail()
     except Exception as exc:
         raise RuntimeError(f"time step {getattr(exc, 'time_index', '?')} failed") from exc
-    return U if device_result else U.cpu().numpy()
+    return U if device_result else to_host(U)
 
 
 def spacetime_residual(spec: ProblemSpec, U, disc: Discretization | None = None):
