@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
   sm.Vt = smem;                    // operand tile (p, or the vector being applied)
   sm.gens = sm.Vt + C::VT;         // generator tables
   sm.red = sm.gens + 6 * C::GL;    // reduction buffers
-  sm.xs = sm.red + C::RED;         // this CTA's part of the CG iterate x
+  sm.xs = sm.red + C::RED;         // this CTA's part of the previous search direction (PCG)
   sm.tabx = sm.xs + C::XS;         // DST sine tables
   sm.taby = sm.tabx + C::ST;
   uint64_t* mbar = reinterpret_cast<uint64_t*>(sm.taby + C::ST);
@@ -202,7 +202,6 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
   double* Vt = sm.Vt;
   double* gens = sm.gens;
   double* red = sm.red;
-  double* xs = sm.xs;
 
   Ctx<C> c;
   c.tid = threadIdx.x;
@@ -272,7 +271,11 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
   const int cid = blockIdx.x / C::G;
   double* sb_ = P.scratch + (size_t)cid * 3 * C::NP * C::NP;  // right-hand side b (true-residual checks)
   double* dinv = sb_ + C::NP * C::NP;                         // 1 / d(s) of the tau preconditioner
-  double* pold_ = dinv + C::NP * C::NP;                       // previous search direction (PCG)
+  // CG iterate x of this CTA's units, fragment-native in the L2-resident scratch: updated with
+  // fire-and-forget reductions (one owner thread per element: ordered, deterministic), read back once
+  // per solve; its shared-memory slot holds the previous search direction instead (critical path)
+  double* xs = dinv + C::NP * C::NP + (size_t)c.rank * C::CU * 256;
+  double* pold_ = sm.xs;
   int buf = 0;
 
   double acc[C::WR][C::NF][4];  // operator output of the current matvec / DST stage
@@ -466,12 +469,12 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           if (j < ny && i < nx) {
             const int xi = elem_xidx<C>(c, mr, nf, e);
             const double pv = Vt[vt_idx<C>(j, i)];
-            xs[xi] = xs[xi] + alpha * pv;
+            atomicAdd(xs + xi, alpha * pv);  // RED: no return value, no latency on the critical path
             const double rn = rr_[mr][nf][e] - alpha * acc[mr][nf][e];
             rr_[mr][nf][e] = rn;
             part2[0][mr][nf >> 1] += rn * rn;
             // the preconditioner overwrites the operand tile: keep p for the direction update
-            if constexpr (PRE) pold_[elem_sidx<C>(c, mr, nf, e)] = pv;
+            if constexpr (PRE) pold_[xi] = pv;
           }
         }
         RM_T(3);
@@ -565,7 +568,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           if (j < ny && i < nx) {
             const int vi = vt_idx<C>(j, i);
             if constexpr (PRE)
-              Vt[vi] = acc[mr][nf][e] + beta * __ldcg(pold_ + elem_sidx<C>(c, mr, nf, e));
+              Vt[vi] = acc[mr][nf][e] + beta * pold_[elem_xidx<C>(c, mr, nf, e)];
             else
               Vt[vi] = rr_[mr][nf][e] + beta * Vt[vi];
           }
