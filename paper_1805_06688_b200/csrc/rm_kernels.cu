@@ -66,24 +66,56 @@ __device__ __forceinline__ int elem_sidx(const Ctx<C>& c, int mr, int nf, int e)
   return (((c.urow + mr) * C::UR + c.ucol + (nf >> 1)) * 256) + (((nf & 1) * 4 + e) * 32) + c.lane;
 }
 
+// Vt <- a (- b): flattened element order, UN independent loads per array in flight per thread
+// (the rows come from HBM or L2; a per-row loop would expose one latency per row)
+template <class C, bool SUB>
+__device__ __forceinline__ void load_rows(double* Vt, const double* __restrict__ a, const double* __restrict__ b,
+                                          int nx, int ny, const Ctx<C>& c) {
+  constexpr int UN = SUB ? 4 : 8;
+  const int ndof = nx * ny;
+  for (int base = c.tid; base < ndof; base += C::THREADS * UN) {
+    double va[UN], vb[UN];
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      const int e = base + u * C::THREADS;
+      va[u] = e < ndof ? __ldcg(a + e) : 0.0;
+      if constexpr (SUB) vb[u] = e < ndof ? __ldcg(b + e) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      const int e = base + u * C::THREADS;
+      if (e < ndof) {
+        const int j = e / nx, i = e - j * nx;
+        Vt[vt_idx<C>(j, i)] = SUB ? va[u] - vb[u] : va[u];
+      }
+    }
+  }
+}
+
 template <class C>
 __device__ __forceinline__ void load_vec(double* Vt, const double* __restrict__ src, int nx, int ny,
                                          const Ctx<C>& c) {
-  for (int j = c.warp; j < ny; j += C::WARPS) {
-    const double* row = src + (int64_t)j * nx;
-    double* dst = Vt + vt_idx<C>(j, 0);
-    for (int i = c.lane; i < nx; i += 32) dst[i] = __ldcg(row + i);
-  }
+  load_rows<C, false>(Vt, src, nullptr, nx, ny, c);
 }
 
 // Vt <- guess - G (G may be null)
 template <class C>
 __device__ __forceinline__ void load_guess(double* Vt, const double* __restrict__ guess, const double* __restrict__ G,
                                            int nx, int ny, const Ctx<C>& c) {
-  for (int j = c.warp; j < ny; j += C::WARPS) {
-    const int64_t o = (int64_t)j * nx;
-    double* dst = Vt + vt_idx<C>(j, 0);
-    for (int i = c.lane; i < nx; i += 32) dst[i] = G ? __ldcg(guess + o + i) - __ldcg(G + o + i) : __ldcg(guess + o + i);
+  if (G)
+    load_rows<C, true>(Vt, guess, G, nx, ny, c);
+  else
+    load_rows<C, false>(Vt, guess, nullptr, nx, ny, c);
+}
+
+// Hint: pull [p, p+bytes) into L2 (TMA bulk prefetch; whole 16-byte granules inside the range only)
+__device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes) {
+  uintptr_t a = ((uintptr_t)p + 15) & ~(uintptr_t)15;
+  const uintptr_t e = ((uintptr_t)p + bytes) & ~(uintptr_t)15;
+  while (a < e) {
+    const uint32_t sz = (uint32_t)min((uintptr_t)32768, e - a);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(sz) : "memory");
+    a += sz;
   }
 }
 
@@ -426,6 +458,19 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           }
         }
         bcast_band<C>(bc, c.rank, c.tid);
+      }
+      if (c.tid == 0 && n < n1) {
+        // the chain's next-step inputs: L2 resident by the time this solve finishes (each CTA of the
+        // group takes a slice of every row)
+        const size_t vb = (size_t)ndof * sizeof(double);
+        const size_t lo = vb * c.rank / C::G, hi = vb * (c.rank + 1) / C::G;
+        auto pf = [&](const double* base, int64_t stride) {
+          if (base) prefetch_l2(reinterpret_cast<const char*>(base + (int64_t)(n + 1) * stride) + lo, hi - lo);
+        };
+        pf(W.d_guess, W.guess_stride);
+        pf(W.d_gadd, W.gadd_stride);
+        pf(W.d_f, W.f_stride);
+        pf(W.d_sub, W.sub_stride);
       }
       RM_T0();
       for (int64_t k = 1; !done; ++k) {
