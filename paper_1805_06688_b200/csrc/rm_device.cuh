@@ -164,10 +164,12 @@ __device__ __forceinline__ void matvec_yseg(const double* __restrict__ Vt, const
 // and the two off-diagonal segments become one contraction of length n+1 (12 n^3 -> 8 n^3 flops).
 // The host sets the bits only when the generators have this property exactly and n % 4 != 0, so
 // that k = n still lies inside the (zero-padded) K range [0, (n+3)&~3) of the plain segments.
-template <class C>
+// mid() runs after the diagonal x segment, which reads only the warp's own rows: callers overlap
+// the arrival of the peers' bands with it.
+template <class C, class Mid>
 __device__ __forceinline__ void matvec(const double* __restrict__ Vt, const double* __restrict__ gens,
                                        double (&acc)[C::WR][C::NF][4], int urow, int ucol, int gq, int tig,
-                                       int kx_end, int ky_end, bool do_x, bool do_y, int merge) {
+                                       int kx_end, int ky_end, bool do_x, bool do_y, int merge, Mid mid) {
 #pragma unroll
   for (int mr = 0; mr < C::WR; ++mr)
 #pragma unroll
@@ -177,12 +179,15 @@ __device__ __forceinline__ void matvec(const double* __restrict__ Vt, const doub
   if (do_x) {
     const double* tab = gens + C::NP + 16 * ucol + gq - tig;
     matvec_xseg<C, false>(Vt, tab, acc, urow, gq, tig, 0, kx_end);
+    mid();
     if (merge & 1) {
       matvec_xseg<C, true>(Vt, tab + C::GL, acc, urow, gq, tig, 1, kx_end);
     } else {
       matvec_xseg<C, false>(Vt, tab + C::GL, acc, urow, gq, tig, 1, kx_end);
       matvec_xseg<C, false>(Vt, tab + 2 * C::GL, acc, urow, gq, tig, -1, kx_end);
     }
+  } else {
+    mid();
   }
   if (do_y) {
     const double* tab = gens + 3 * C::GL + C::NP - tig;
@@ -194,6 +199,13 @@ __device__ __forceinline__ void matvec(const double* __restrict__ Vt, const doub
       matvec_yseg<C, false>(Vt, tab + 2 * C::GL, acc, urow, ucol, gq, tig, -1, ky_end);
     }
   }
+}
+
+template <class C>
+__device__ __forceinline__ void matvec(const double* __restrict__ Vt, const double* __restrict__ gens,
+                                       double (&acc)[C::WR][C::NF][4], int urow, int ucol, int gq, int tig,
+                                       int kx_end, int ky_end, bool do_x, bool do_y, int merge) {
+  matvec<C>(Vt, gens, acc, urow, ucol, gq, tig, kx_end, ky_end, do_x, do_y, merge, [] {});
 }
 
 // ----------------------------------------------------------------------------
@@ -435,9 +447,10 @@ __device__ __forceinline__ uint32_t bcast_seg_off(int rank, int t) {
   }
 }
 
-// Call after this CTA's threads wrote their elements of Vt (own band only).
+// Call after this CTA's threads wrote their elements of Vt (own band only): pushes the band to every
+// peer (bcast_wait then waits for the peers' bands).
 template <class C>
-__device__ __forceinline__ void bcast_band(Bcast<C>& b, int rank, int tid) {
+__device__ __forceinline__ void bcast_issue(Bcast<C>& b, int rank, int tid) {
   if constexpr (C::G == 1) {
     __syncthreads();
   } else {
@@ -460,6 +473,12 @@ __device__ __forceinline__ void bcast_band(Bcast<C>& b, int rank, int tid) {
             : "memory");
       }
     }
+  }
+}
+
+template <class C>
+__device__ __forceinline__ void bcast_wait(Bcast<C>& b) {
+  if constexpr (C::G > 1) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tLAB_WAIT:\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
@@ -468,6 +487,12 @@ __device__ __forceinline__ void bcast_band(Bcast<C>& b, int rank, int tid) {
         : "memory");
     b.phase ^= 1;
   }
+}
+
+template <class C>
+__device__ __forceinline__ void bcast_band(Bcast<C>& b, int rank, int tid) {
+  bcast_issue<C>(b, rank, tid);
+  bcast_wait<C>(b);
 }
 
 // Deterministic group-wide sum of NV values.  part[v][mr][uc] is this

@@ -208,10 +208,13 @@ __device__ __forceinline__ void apply_tau(const Ctx<C>& c, const Smem<C>& sm, Bc
     dst_y<C>(Vt, sm.taby, Ly, acc, c.urow, c.ucol, c.gq, c.tig, ky_end, fold_y);
     RM_T(11);
     if (pass == 1) break;
+    // diagonal scaling: the dinv loads are issued before the barrier, which hides their L2 latency
+    double dv[C::WR][C::NF][4];
+    RM_FOR_ELEM { dv[mr][nf][e] = __ldcg(dinv + elem_sidx<C>(c, mr, nf, e)); }
     group_sync<C::G>();  // every CTA done reading its tile before peers push the next band
     RM_FOR_ELEM {
       const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
-      if (j < ny && i < nx) Vt[vt_idx<C>(j, i)] = acc[mr][nf][e] * __ldcg(dinv + elem_sidx<C>(c, mr, nf, e));
+      if (j < ny && i < nx) Vt[vt_idx<C>(j, i)] = acc[mr][nf][e] * dv[mr][nf][e];
     }
     __syncthreads();
     RM_T(12);
@@ -457,7 +460,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
             if (j < ny && i < nx) Vt[vt_idx<C>(j, i)] = rr_[mr][nf][e];
           }
         }
-        bcast_band<C>(bc, c.rank, c.tid);
+        bcast_issue<C>(bc, c.rank, c.tid);  // waited for inside the first matvec
       }
       if (c.tid == 0 && n < n1) {
         // the chain's next-step inputs: L2 resident by the time this solve finishes (each CTA of the
@@ -475,13 +478,17 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
       RM_T0();
       for (int64_t k = 1; !done; ++k) {
         if (k > max_iter) {
+          bcast_wait<C>(bc);  // complete the pending exchange (keeps the mbarrier phase in step)
           fail = RM_CG_BUDGET;
           its = max_iter;
           break;
         }
         RM_T(7);
-        // Ap and p'Ap
-        matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true, P.merge);
+        // Ap and p'Ap; the peers' bands of p arrive during the diagonal x segment (own rows only)
+        if constexpr (C::G > C::UR) bcast_wait<C>(bc);  // own rows are shared: nothing to overlap
+        matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true, P.merge, [&] {
+          if constexpr (C::G <= C::UR) bcast_wait<C>(bc);
+        });
         ++nmv;
         RM_T(0);
         double p1[1][C::WR][C::WC];
@@ -602,7 +609,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
             const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
             if (j < ny && i < nx) Vt[vt_idx<C>(j, i)] = acc[mr][nf][e];
           }
-          bcast_band<C>(bc, c.rank, c.tid);
+          bcast_issue<C>(bc, c.rank, c.tid);
           continue;
         }
         const double rho_new = red2[1];
@@ -619,7 +626,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           }
         }
         RM_T(5);
-        bcast_band<C>(bc, c.rank, c.tid);
+        bcast_issue<C>(bc, c.rank, c.tid);
         RM_T(6);
       }
 
