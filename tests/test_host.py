@@ -202,3 +202,25 @@ def test_sweep_struct_layout_matches_header(tmp_path):
     got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
     want = [getattr(_native.Sweep, f).offset for f in fields] + [ctypes.sizeof(_native.Sweep)]
     assert got == want
+
+
+def test_trace_payload_schema(tmp_path):
+    """reporting.py:59-75 schema: keys, types, quarantined timing, factor only with >= 6 norms."""
+    import json
+
+    from paper_1805_06688_b200.mgrit import IterationTrace
+    from paper_1805_06688_b200.reporting import trace_payload, write_trace
+
+    tr = IterationTrace(residual_norms=[81.0, 9.0, 1.0, 0.1, 1e-2, 1e-3, 1e-4], spatial_solves=[10, 20, 30, 40, 50, 60, 70],
+                        cg_iterations=[100, 200, 300, 400, 500, 600, 700], wall_times=[0.0] * 7, seed=0, converged=True)
+    p = trace_payload(tr, {"config": "cfg1"})
+    assert set(p) == {"config", "seed", "converged", "iterations", "residual_norms", "spatial_solves",
+                      "cg_iterations", "timing", "convergence_factor"}
+    assert p["iterations"] == 6 and p["timing"] == {"wall_times": [0.0] * 7}
+    assert abs(p["convergence_factor"] - (1e-4 / 9.0) ** 0.2) < 1e-15
+    short = IterationTrace(residual_norms=[1.0, 0.5], spatial_solves=[1, 2], cg_iterations=[3, 4])
+    assert "convergence_factor" not in trace_payload(short, {})
+    out = write_trace(tmp_path / "sub" / "trace.json", tr, {"b": 1, "a": 2})
+    text = out.read_text()
+    assert text.endswith("\n") and json.loads(text) == json.loads(json.dumps(p | {"config": {"b": 1, "a": 2}}))
+    assert text.index('"cg_iterations"') < text.index('"config"')  # sort_keys=True
