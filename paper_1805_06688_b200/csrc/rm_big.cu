@@ -35,11 +35,13 @@ struct BigCfg {
   static constexpr int SP = NP + 16;       // PV row stride (doubles)
   static constexpr int PV = (NP + 2) * SP; // PV vector size (doubles)
   static constexpr int GL = 2 * NP + 8;    // generator / sine table length
-  static constexpr int XS = 36;            // x-stage row stride (== 4 mod 16)
+  static constexpr int XS = 34;            // x-stage row stride (== 2 mod 16: rows 2 apart conflict-free)
   static constexpr int XROWS = 130;
   static constexpr int YS = 148;           // y-stage row stride (== 4 mod 16)
   static constexpr int YCOLS = 144;        // C0-8 .. C0+135
-  static constexpr int STAGE = (XROWS * XS > 33 * YS ? XROWS * XS : 33 * YS);  // doubles per stage
+  static constexpr int CHUNK = (XROWS * XS > 33 * YS ? XROWS * XS : 33 * YS);  // doubles per chunk
+  static constexpr int STAGE = 2 * CHUNK;  // a chunk and (folded DST) its mirror
+  static constexpr int HALF = NP / 2;
   static constexpr int TE = 128 * 128;     // elements per tile
   static constexpr size_t SMEM = sizeof(double) * (6 * GL + 2 * GL + 2 * STAGE + 4 * 64 + 2 * 4 * 16) + 64;
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
@@ -51,8 +53,14 @@ struct BigCtx {
   int wr, wc0;  // warp strip: unit row wr (0..7), first unit column wc0 (0 or 4)
 };
 
+// Row r (0..15) of unit row ur inside a tile: parity-interleaved in 32-row blocks, so that every
+// MMA fragment of the folded y-DST has outputs of one parity (one K operand, see rm_device.cuh).
+__device__ __forceinline__ int big_urow(int ur, int r) { return 32 * (ur >> 1) + (ur & 1) + 2 * r; }
+
 // element of (nf, e) in the normal mapping, tile coordinates added
-__device__ __forceinline__ int big_row(const BigCtx& c, int e) { return c.R0 + 16 * c.wr + c.gq + 8 * (e >> 1); }
+__device__ __forceinline__ int big_row(const BigCtx& c, int e) {
+  return c.R0 + big_urow(c.wr, c.gq + 8 * (e >> 1));
+}
 __device__ __forceinline__ int big_col(const BigCtx& c, int nf, int e) {
   return c.C0 + 16 * c.wc0 + 8 * nf + 2 * c.tig + (e & 1);
 }
@@ -60,7 +68,11 @@ __device__ __forceinline__ int big_col(const BigCtx& c, int nf, int e) {
 __device__ __forceinline__ int bigT_row(const BigCtx& c, int nf, int e) {
   return c.R0 + 16 * c.wc0 + 8 * nf + 2 * c.tig + (e & 1);
 }
-__device__ __forceinline__ int bigT_col(const BigCtx& c, int e) { return c.C0 + 16 * c.wr + c.gq + 8 * (e >> 1); }
+// output column of the transposed stage; folded: m-tiles 0..3 give the even columns (u half, alpha odd),
+// 4..7 the odd ones (w half) of the tile
+__device__ __forceinline__ int bigT_col(const BigCtx& c, int e, bool fold) {
+  return fold ? c.C0 + 32 * (c.wr & 3) + 2 * c.gq + 16 * (e >> 1) + (c.wr >> 2) : c.C0 + 16 * c.wr + c.gq + 8 * (e >> 1);
+}
 // fragment-native index of (nf, e) inside the CTA's scratch vectors
 __device__ __forceinline__ int big_fidx(const BigCtx& c, int nf, int e) {
   return ((c.warp * 8 + nf) * 4 + e) * 32 + c.lane;
@@ -126,12 +138,12 @@ __device__ __forceinline__ void big_matvec(const double* __restrict__ pv, const 
     for (int seg = 0; seg < ((merge & 1) ? 2 : 3); ++seg) {
       const int delta = seg == 0 ? 0 : (seg == 1 ? 1 : -1);
       const double* tab = gens + seg * C::GL + C::NP + c.C0 + 16 * c.wc0 + c.gq - c.tig - k0;
-      const double* ar = s + (16 * c.wr + c.gq + delta + 1) * C::XS + c.tig + 2;
+      const double* ar = s + (big_urow(c.wr, c.gq) + delta + 1) * C::XS + c.tig + 2;
       if (seg == 1 && (merge & 1)) {  // T2 (V[j+1][k] + V[j-1][k-1]), see rm_device.cuh matvec
-        const double* am = s + (16 * c.wr + c.gq) * C::XS + c.tig + 1;
+        const double* am = s + big_urow(c.wr, c.gq) * C::XS + c.tig + 1;
 #pragma unroll 4
         for (int k = 0; k < 32; k += 4) {
-          const double a0 = ar[k] + am[k], a1 = ar[k + 8 * C::XS] + am[k + 8 * C::XS];
+          const double a0 = ar[k] + am[k], a1 = ar[k + 16 * C::XS] + am[k + 16 * C::XS];
           double b[8];
 #pragma unroll
           for (int nf = 0; nf < 8; ++nf) b[nf] = tab[8 * nf - k];
@@ -142,7 +154,7 @@ __device__ __forceinline__ void big_matvec(const double* __restrict__ pv, const 
       }
 #pragma unroll 4
       for (int k = 0; k < 32; k += 4) {
-        const double a0 = ar[k], a1 = ar[k + 8 * C::XS];
+        const double a0 = ar[k], a1 = ar[k + 16 * C::XS];
         double b[8];
 #pragma unroll
         for (int nf = 0; nf < 8; ++nf) b[nf] = tab[8 * nf - k];
@@ -166,13 +178,13 @@ __device__ __forceinline__ void big_matvec(const double* __restrict__ pv, const 
 #pragma unroll 1
     for (int seg = 0; seg < ((merge & 2) ? 2 : 3); ++seg) {
       const int delta = seg == 0 ? 0 : (seg == 1 ? 1 : -1);
-      const double* tab = gens + (3 + seg) * C::GL + C::NP + c.R0 + 16 * c.wr + c.gq - c.tig - l0;
+      const double* tab = gens + (3 + seg) * C::GL + C::NP + c.R0 + big_urow(c.wr, c.gq) - c.tig - l0;
       const double* br = s + (c.tig + 1) * C::YS + 16 * c.wc0 + c.gq + delta + 8;
       if (seg == 1 && (merge & 2)) {  // T2 (V[l][i+1] + V[l-1][i-1])
         const double* bm = s + c.tig * C::YS + 16 * c.wc0 + c.gq + 7;
 #pragma unroll 4
         for (int l = 0; l < 32; l += 4) {
-          const double a0 = tab[-l], a1 = tab[8 - l];
+          const double a0 = tab[-l], a1 = tab[16 - l];
           double b[8];
 #pragma unroll
           for (int nf = 0; nf < 8; ++nf) b[nf] = br[l * C::YS + 8 * nf] + bm[l * C::YS + 8 * nf];
@@ -183,7 +195,7 @@ __device__ __forceinline__ void big_matvec(const double* __restrict__ pv, const 
       }
 #pragma unroll 4
       for (int l = 0; l < 32; l += 4) {
-        const double a0 = tab[-l], a1 = tab[8 - l];
+        const double a0 = tab[-l], a1 = tab[16 - l];
         double b[8];
 #pragma unroll
         for (int nf = 0; nf < 8; ++nf) b[nf] = br[l * C::YS + 8 * nf];
@@ -195,77 +207,138 @@ __device__ __forceinline__ void big_matvec(const double* __restrict__ pv, const 
   }
 }
 
-// DST along x in the transposed mapping: out^T[i][j] = sum_k Sx[i][k] V[j][k]
+// DST along x in the transposed mapping: out^T[i][j] = sum_k Sx[i][k] V[j][k].  Folded (n = NP-1, see
+// rm_device.cuh): K runs over k < HALF with the B operand v_k +- v_{NP-2-k}; every K chunk streams its
+// mirror chunk (columns NP-34-k0 .. NP-1-k0) next to it; output columns per bigT_col.
 template <class C>
 __device__ __forceinline__ void big_dst_xT(const double* __restrict__ pv, const double* __restrict__ tab, int L,
-                                           double* stage, double (&acc)[8][4], const BigCtx& c, int kx_end) {
+                                           double* stage, double (&acc)[8][4], const BigCtx& c, int kx_end,
+                                           bool fold) {
 #pragma unroll
   for (int nf = 0; nf < 8; ++nf)
 #pragma unroll
     for (int e = 0; e < 4; ++e) acc[nf][e] = 0.0;
   double* st[2] = {stage, stage + C::STAGE};
-  const int nkx = kx_end / 32 + ((kx_end & 31) ? 1 : 0);
-  const int xa = c.C0 + 16 * c.wr + c.gq + 1, xb = xa + 8;
+  const int kend = fold ? C::HALF : kx_end;
+  const int nkx = kend / 32 + ((kend & 31) ? 1 : 0);
+  const int xa = bigT_col(c, 0, fold) + 1, xb = bigT_col(c, 2, fold) + 1;  // alpha of rows gq, gq+8
   int ia = (xa * (c.tig + 1)) % L, ib = (xb * (c.tig + 1)) % L;
   const int sa = (4 * xa) % L, sb = (4 * xb) % L;
+  const bool w = c.wr >= 4;
+  const double sgn = w ? -1.0 : 1.0;
+  const double sgn_last = (c.tig == 3) ? (w ? -1.0 : 0.0) : sgn;
   load_xchunk<C>(st[0], pv, c.R0, 0, c.tid);
+  if (fold) load_xchunk<C>(st[0] + C::CHUNK, pv, c.R0, C::NP - 32, c.tid);
   cp_async_commit();
   for (int ch = 0; ch < nkx; ++ch) {
-    if (ch + 1 < nkx) load_xchunk<C>(st[(ch + 1) & 1], pv, c.R0, 32 * (ch + 1), c.tid);
+    if (ch + 1 < nkx) {
+      load_xchunk<C>(st[(ch + 1) & 1], pv, c.R0, 32 * (ch + 1), c.tid);
+      if (fold) load_xchunk<C>(st[(ch + 1) & 1] + C::CHUNK, pv, c.R0, C::NP - 32 - 32 * (ch + 1), c.tid);
+    }
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
     const double* br = st[ch & 1] + (16 * c.wc0 + c.gq + 1) * C::XS + c.tig + 2;
+    if (fold) {
+      // partner column NP-2-k of k = k0 + kk sits at mirror offset 32 - kk (chunk column index)
+      const double* bm = st[ch & 1] + C::CHUNK + (16 * c.wc0 + c.gq + 1) * C::XS + 32 - c.tig;
+      const bool last_chunk = 32 * ch + 32 >= C::HALF;
 #pragma unroll 4
-    for (int k = 0; k < 32; k += 4) {
-      const double a0 = tab[ia], a1 = tab[ib];
-      double b[8];
+      for (int k = 0; k < 32; k += 4) {
+        const double a0 = tab[ia], a1 = tab[ib];
+        const double f = (last_chunk && k == 28) ? sgn_last : sgn;
+        double b[8];
 #pragma unroll
-      for (int nf = 0; nf < 8; ++nf) b[nf] = br[8 * nf * C::XS + k];
+        for (int nf = 0; nf < 8; ++nf) b[nf] = fma(f, bm[8 * nf * C::XS - k], br[8 * nf * C::XS + k]);
 #pragma unroll
-      for (int nf = 0; nf < 8; ++nf) dmma(acc[nf], a0, a1, b[nf]);
-      ia += sa;
-      ia -= ia >= L ? L : 0;
-      ib += sb;
-      ib -= ib >= L ? L : 0;
+        for (int nf = 0; nf < 8; ++nf) dmma(acc[nf], a0, a1, b[nf]);
+        ia += sa;
+        ia -= ia >= L ? L : 0;
+        ib += sb;
+        ib -= ib >= L ? L : 0;
+      }
+    } else {
+#pragma unroll 4
+      for (int k = 0; k < 32; k += 4) {
+        const double a0 = tab[ia], a1 = tab[ib];
+        double b[8];
+#pragma unroll
+        for (int nf = 0; nf < 8; ++nf) b[nf] = br[8 * nf * C::XS + k];
+#pragma unroll
+        for (int nf = 0; nf < 8; ++nf) dmma(acc[nf], a0, a1, b[nf]);
+        ia += sa;
+        ia -= ia >= L ? L : 0;
+        ib += sb;
+        ib -= ib >= L ? L : 0;
+      }
     }
     __syncthreads();
   }
 }
 
-// DST along y in the normal mapping: out[j][i] = sum_l Sy[j][l] V[l][i]
+// DST along y in the normal mapping: out[j][i] = sum_l Sy[j][l] V[l][i].  Folded: K over l < HALF with
+// v_l +- v_{NP-2-l} (u for even unit rows = alpha odd, w for odd ones); mirror rows NP-34-l0 .. NP-2-l0.
 template <class C>
 __device__ __forceinline__ void big_dst_y(const double* __restrict__ pv, const double* __restrict__ tab, int L,
-                                          double* stage, double (&acc)[8][4], const BigCtx& c, int ky_end) {
+                                          double* stage, double (&acc)[8][4], const BigCtx& c, int ky_end,
+                                          bool fold) {
 #pragma unroll
   for (int nf = 0; nf < 8; ++nf)
 #pragma unroll
     for (int e = 0; e < 4; ++e) acc[nf][e] = 0.0;
   double* st[2] = {stage, stage + C::STAGE};
-  const int nky = ky_end / 32 + ((ky_end & 31) ? 1 : 0);
-  const int ja = c.R0 + 16 * c.wr + c.gq + 1, jb = ja + 8;
+  const int kend = fold ? C::HALF : ky_end;
+  const int nky = kend / 32 + ((kend & 31) ? 1 : 0);
+  const int ja = big_row(c, 0) + 1, jb = big_row(c, 2) + 1;
   int ia = (ja * (c.tig + 1)) % L, ib = (jb * (c.tig + 1)) % L;
   const int sa = (4 * ja) % L, sb = (4 * jb) % L;
+  const bool w = c.wr & 1;
+  const double sgn = w ? -1.0 : 1.0;
+  const double sgn_last = (c.tig == 3) ? (w ? -1.0 : 0.0) : sgn;
   load_ychunk<C>(st[0], pv, 0, c.C0, c.tid);
+  if (fold) load_ychunk<C>(st[0] + C::CHUNK, pv, C::NP - 33, c.C0, c.tid);
   cp_async_commit();
   for (int ch = 0; ch < nky; ++ch) {
-    if (ch + 1 < nky) load_ychunk<C>(st[(ch + 1) & 1], pv, 32 * (ch + 1), c.C0, c.tid);
+    if (ch + 1 < nky) {
+      load_ychunk<C>(st[(ch + 1) & 1], pv, 32 * (ch + 1), c.C0, c.tid);
+      if (fold) load_ychunk<C>(st[(ch + 1) & 1] + C::CHUNK, pv, C::NP - 33 - 32 * (ch + 1), c.C0, c.tid);
+    }
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
     const double* br = st[ch & 1] + (c.tig + 1) * C::YS + 16 * c.wc0 + c.gq + 8;
+    if (fold) {
+      // partner row NP-2-l of l = l0 + ll sits at mirror row 32 - ll
+      const double* bm = st[ch & 1] + C::CHUNK + (32 - c.tig) * C::YS + 16 * c.wc0 + c.gq + 8;
+      const bool last_chunk = 32 * ch + 32 >= C::HALF;
 #pragma unroll 4
-    for (int l = 0; l < 32; l += 4) {
-      const double a0 = tab[ia], a1 = tab[ib];
-      double b[8];
+      for (int l = 0; l < 32; l += 4) {
+        const double a0 = tab[ia], a1 = tab[ib];
+        const double f = (last_chunk && l == 28) ? sgn_last : sgn;
+        double b[8];
 #pragma unroll
-      for (int nf = 0; nf < 8; ++nf) b[nf] = br[l * C::YS + 8 * nf];
+        for (int nf = 0; nf < 8; ++nf) b[nf] = fma(f, bm[8 * nf - l * C::YS], br[l * C::YS + 8 * nf]);
 #pragma unroll
-      for (int nf = 0; nf < 8; ++nf) dmma(acc[nf], a0, a1, b[nf]);
-      ia += sa;
-      ia -= ia >= L ? L : 0;
-      ib += sb;
-      ib -= ib >= L ? L : 0;
+        for (int nf = 0; nf < 8; ++nf) dmma(acc[nf], a0, a1, b[nf]);
+        ia += sa;
+        ia -= ia >= L ? L : 0;
+        ib += sb;
+        ib -= ib >= L ? L : 0;
+      }
+    } else {
+#pragma unroll 4
+      for (int l = 0; l < 32; l += 4) {
+        const double a0 = tab[ia], a1 = tab[ib];
+        double b[8];
+#pragma unroll
+        for (int nf = 0; nf < 8; ++nf) b[nf] = br[l * C::YS + 8 * nf];
+#pragma unroll
+        for (int nf = 0; nf < 8; ++nf) dmma(acc[nf], a0, a1, b[nf]);
+        ia += sa;
+        ia -= ia >= L ? L : 0;
+        ib += sb;
+        ib -= ib >= L ? L : 0;
+      }
     }
     __syncthreads();
   }
@@ -357,6 +430,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
   const double cm = P.cm;
   const int64_t max_iter = W.max_iter > 0 ? W.max_iter : 10 * (int64_t)ndof;
   const bool need_in = W.explicit_rhs || W.x0_mode == 1;
+  const bool fold_x = nx == C::NP - 1, fold_y = ny == C::NP - 1;  // even/odd folded DST stages
 
   if constexpr (PRE) {
     for (int i = c.tid; i < Lx; i += C::THREADS) tabx[i] = P.tabx[i];
@@ -528,13 +602,13 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
         group_sync<C::G>();
 #pragma unroll 1
         for (int pass = 0; pass < 2; ++pass) {
-          big_dst_xT<C>(pv1, tabx, Lx, stage, acc, c, kx_end);
+          big_dst_xT<C>(pv1, tabx, Lx, stage, acc, c, kx_end, fold_x);
           RM_BIG_FOR {
-            const int j = bigT_row(c, nf, e), i = bigT_col(c, e);
+            const int j = bigT_row(c, nf, e), i = bigT_col(c, e, fold_x);
             if (j < ny && i < nx) put_tile(pv0, j, i, acc[nf][e]);
           }
           group_sync<C::G>();
-          big_dst_y<C>(pv0, taby, Ly, stage, acc, c, ky_end);
+          big_dst_y<C>(pv0, taby, Ly, stage, acc, c, ky_end, fold_y);
           if (pass == 1) break;
           RM_BIG_FOR {
             const int j = big_row(c, e), i = big_col(c, nf, e);
