@@ -35,11 +35,16 @@ struct BigCfg {
   static constexpr int SP = NP + 16;       // PV row stride (doubles)
   static constexpr int PV = (NP + 2) * SP; // PV vector size (doubles)
   static constexpr int GL = 2 * NP + 8;    // generator / sine table length
-  static constexpr int XS = 34;            // x-stage row stride (== 2 mod 16: rows 2 apart conflict-free)
+  // K chunk width: 32, or 16 at NP = 1024 (the generator/sine tables take 129 KB of shared memory)
+  static constexpr int KC = NP > 512 ? 16 : 32;
+  static constexpr int XS = KC + 2;        // x-stage row stride (== 2 mod 16: rows 2 apart conflict-free)
   static constexpr int XROWS = 130;
   static constexpr int YS = 148;           // y-stage row stride (== 4 mod 16)
   static constexpr int YCOLS = 144;        // C0-8 .. C0+135
-  static constexpr int CHUNK = (XROWS * XS > 33 * YS ? XROWS * XS : 33 * YS);  // doubles per chunk
+  static constexpr int CHUNK = (XROWS * XS > (KC + 1) * YS ? XROWS * XS : (KC + 1) * YS);  // doubles per chunk
+  // more than 16 CTAs per chain (NP = 1024: 64) exceed the cluster limit: the chain's CTAs then
+  // synchronise through global memory (co-resident by a cooperative launch) instead of cluster barriers
+  static constexpr bool GSYNC = G > 16;
   static constexpr int STAGE = 2 * CHUNK;  // a chunk and (folded DST) its mirror
   static constexpr int HALF = NP / 2;
   static constexpr int TE = 128 * 128;     // elements per tile
@@ -98,16 +103,17 @@ __device__ __forceinline__ void cp_async_wait() {
 // ---- chunk loaders (all threads) ------------------------------------------------------
 template <class C>
 __device__ __forceinline__ void load_xchunk(double* st, const double* __restrict__ pv, int R0, int k0, int tid) {
-  // rows R0-1 .. R0+128 (130), cols k0-2 .. k0+31 (17 x 16B per row; column k0-1 for the merged segment)
-  for (int t = tid; t < C::XROWS * 17; t += C::THREADS) {
-    const int r = t / 17, q = t % 17;
+  // rows R0-1 .. R0+128 (130), cols k0-2 .. k0+KC-1 (KC/2+1 x 16B per row; column k0-1 for the merged segment)
+  constexpr int QR = C::KC / 2 + 1;
+  for (int t = tid; t < C::XROWS * QR; t += C::THREADS) {
+    const int r = t / QR, q = t % QR;
     cp_async16(st + r * C::XS + 2 * q, pv + pv_idx<C>(R0 - 1 + r, k0 - 2) + 2 * q);
   }
 }
 template <class C>
 __device__ __forceinline__ void load_ychunk(double* st, const double* __restrict__ pv, int l0, int C0, int tid) {
-  // rows l0-1 .. l0+31 (row l0-1 for the merged segment), cols C0-8 .. C0+135 (72 x 16B per row)
-  for (int t = tid; t < 33 * 72; t += C::THREADS) {
+  // rows l0-1 .. l0+KC-1 (row l0-1 for the merged segment), cols C0-8 .. C0+135 (72 x 16B per row)
+  for (int t = tid; t < (C::KC + 1) * 72; t += C::THREADS) {
     const int r = t / 72, q = t % 72;
     cp_async16(st + r * C::YS + 2 * q, pv + pv_idx<C>(l0 - 1 + r, C0 - 8) + 2 * q);
   }
@@ -124,16 +130,16 @@ __device__ __forceinline__ void big_matvec(const double* __restrict__ pv, const 
     for (int e = 0; e < 4; ++e) acc[nf][e] = 0.0;
   double* st[2] = {stage, stage + C::STAGE};
   // ---- x-part: K = columns
-  const int nkx = kx_end / 32 + ((kx_end & 31) ? 1 : 0);
+  const int nkx = (kx_end + C::KC - 1) / C::KC;
   load_xchunk<C>(st[0], pv, c.R0, 0, c.tid);
   cp_async_commit();
   for (int ch = 0; ch < nkx; ++ch) {
-    if (ch + 1 < nkx) load_xchunk<C>(st[(ch + 1) & 1], pv, c.R0, 32 * (ch + 1), c.tid);
+    if (ch + 1 < nkx) load_xchunk<C>(st[(ch + 1) & 1], pv, c.R0, C::KC * (ch + 1), c.tid);
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
     const double* s = st[ch & 1];
-    const int k0 = 32 * ch;
+    const int k0 = C::KC * ch;
 #pragma unroll 1
     for (int seg = 0; seg < ((merge & 1) ? 2 : 3); ++seg) {
       const int delta = seg == 0 ? 0 : (seg == 1 ? 1 : -1);
@@ -142,7 +148,7 @@ __device__ __forceinline__ void big_matvec(const double* __restrict__ pv, const 
       if (seg == 1 && (merge & 1)) {  // T2 (V[j+1][k] + V[j-1][k-1]), see rm_device.cuh matvec
         const double* am = s + big_urow(c.wr, c.gq) * C::XS + c.tig + 1;
 #pragma unroll 4
-        for (int k = 0; k < 32; k += 4) {
+        for (int k = 0; k < C::KC; k += 4) {
           const double a0 = ar[k] + am[k], a1 = ar[k + 16 * C::XS] + am[k + 16 * C::XS];
           double b[8];
 #pragma unroll
@@ -153,7 +159,7 @@ __device__ __forceinline__ void big_matvec(const double* __restrict__ pv, const 
         continue;
       }
 #pragma unroll 4
-      for (int k = 0; k < 32; k += 4) {
+      for (int k = 0; k < C::KC; k += 4) {
         const double a0 = ar[k], a1 = ar[k + 16 * C::XS];
         double b[8];
 #pragma unroll
@@ -165,16 +171,16 @@ __device__ __forceinline__ void big_matvec(const double* __restrict__ pv, const 
     __syncthreads();
   }
   // ---- y-part: K = rows
-  const int nky = ky_end / 32 + ((ky_end & 31) ? 1 : 0);
+  const int nky = (ky_end + C::KC - 1) / C::KC;
   load_ychunk<C>(st[0], pv, 0, c.C0, c.tid);
   cp_async_commit();
   for (int ch = 0; ch < nky; ++ch) {
-    if (ch + 1 < nky) load_ychunk<C>(st[(ch + 1) & 1], pv, 32 * (ch + 1), c.C0, c.tid);
+    if (ch + 1 < nky) load_ychunk<C>(st[(ch + 1) & 1], pv, C::KC * (ch + 1), c.C0, c.tid);
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
     const double* s = st[ch & 1];
-    const int l0 = 32 * ch;
+    const int l0 = C::KC * ch;
 #pragma unroll 1
     for (int seg = 0; seg < ((merge & 2) ? 2 : 3); ++seg) {
       const int delta = seg == 0 ? 0 : (seg == 1 ? 1 : -1);
@@ -183,7 +189,7 @@ __device__ __forceinline__ void big_matvec(const double* __restrict__ pv, const 
       if (seg == 1 && (merge & 2)) {  // T2 (V[l][i+1] + V[l-1][i-1])
         const double* bm = s + c.tig * C::YS + 16 * c.wc0 + c.gq + 7;
 #pragma unroll 4
-        for (int l = 0; l < 32; l += 4) {
+        for (int l = 0; l < C::KC; l += 4) {
           const double a0 = tab[-l], a1 = tab[16 - l];
           double b[8];
 #pragma unroll
@@ -194,7 +200,7 @@ __device__ __forceinline__ void big_matvec(const double* __restrict__ pv, const 
         continue;
       }
 #pragma unroll 4
-      for (int l = 0; l < 32; l += 4) {
+      for (int l = 0; l < C::KC; l += 4) {
         const double a0 = tab[-l], a1 = tab[16 - l];
         double b[8];
 #pragma unroll
@@ -209,7 +215,7 @@ __device__ __forceinline__ void big_matvec(const double* __restrict__ pv, const 
 
 // DST along x in the transposed mapping: out^T[i][j] = sum_k Sx[i][k] V[j][k].  Folded (n = NP-1, see
 // rm_device.cuh): K runs over k < HALF with the B operand v_k +- v_{NP-2-k}; every K chunk streams its
-// mirror chunk (columns NP-34-k0 .. NP-1-k0) next to it; output columns per bigT_col.
+// mirror chunk (columns NP-KC-2-k0 .. NP-1-k0) next to it; output columns per bigT_col.
 template <class C>
 __device__ __forceinline__ void big_dst_xT(const double* __restrict__ pv, const double* __restrict__ tab, int L,
                                            double* stage, double (&acc)[8][4], const BigCtx& c, int kx_end,
@@ -220,7 +226,7 @@ __device__ __forceinline__ void big_dst_xT(const double* __restrict__ pv, const 
     for (int e = 0; e < 4; ++e) acc[nf][e] = 0.0;
   double* st[2] = {stage, stage + C::STAGE};
   const int kend = fold ? C::HALF : kx_end;
-  const int nkx = kend / 32 + ((kend & 31) ? 1 : 0);
+  const int nkx = (kend + C::KC - 1) / C::KC;
   const int xa = bigT_col(c, 0, fold) + 1, xb = bigT_col(c, 2, fold) + 1;  // alpha of rows gq, gq+8
   int ia = (xa * (c.tig + 1)) % L, ib = (xb * (c.tig + 1)) % L;
   const int sa = (4 * xa) % L, sb = (4 * xb) % L;
@@ -228,25 +234,25 @@ __device__ __forceinline__ void big_dst_xT(const double* __restrict__ pv, const 
   const double sgn = w ? -1.0 : 1.0;
   const double sgn_last = (c.tig == 3) ? (w ? -1.0 : 0.0) : sgn;
   load_xchunk<C>(st[0], pv, c.R0, 0, c.tid);
-  if (fold) load_xchunk<C>(st[0] + C::CHUNK, pv, c.R0, C::NP - 32, c.tid);
+  if (fold) load_xchunk<C>(st[0] + C::CHUNK, pv, c.R0, C::NP - C::KC, c.tid);
   cp_async_commit();
   for (int ch = 0; ch < nkx; ++ch) {
     if (ch + 1 < nkx) {
-      load_xchunk<C>(st[(ch + 1) & 1], pv, c.R0, 32 * (ch + 1), c.tid);
-      if (fold) load_xchunk<C>(st[(ch + 1) & 1] + C::CHUNK, pv, c.R0, C::NP - 32 - 32 * (ch + 1), c.tid);
+      load_xchunk<C>(st[(ch + 1) & 1], pv, c.R0, C::KC * (ch + 1), c.tid);
+      if (fold) load_xchunk<C>(st[(ch + 1) & 1] + C::CHUNK, pv, c.R0, C::NP - C::KC - C::KC * (ch + 1), c.tid);
     }
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
     const double* br = st[ch & 1] + (16 * c.wc0 + c.gq + 1) * C::XS + c.tig + 2;
     if (fold) {
-      // partner column NP-2-k of k = k0 + kk sits at mirror offset 32 - kk (chunk column index)
-      const double* bm = st[ch & 1] + C::CHUNK + (16 * c.wc0 + c.gq + 1) * C::XS + 32 - c.tig;
-      const bool last_chunk = 32 * ch + 32 >= C::HALF;
+      // partner column NP-2-k of k = k0 + kk sits at mirror offset KC - kk (chunk column index)
+      const double* bm = st[ch & 1] + C::CHUNK + (16 * c.wc0 + c.gq + 1) * C::XS + C::KC - c.tig;
+      const bool last_chunk = C::KC * ch + C::KC >= C::HALF;
 #pragma unroll 4
-      for (int k = 0; k < 32; k += 4) {
+      for (int k = 0; k < C::KC; k += 4) {
         const double a0 = tab[ia], a1 = tab[ib];
-        const double f = (last_chunk && k == 28) ? sgn_last : sgn;
+        const double f = (last_chunk && k == C::KC - 4) ? sgn_last : sgn;
         double b[8];
 #pragma unroll
         for (int nf = 0; nf < 8; ++nf) b[nf] = fma(f, bm[8 * nf * C::XS - k], br[8 * nf * C::XS + k]);
@@ -259,7 +265,7 @@ __device__ __forceinline__ void big_dst_xT(const double* __restrict__ pv, const 
       }
     } else {
 #pragma unroll 4
-      for (int k = 0; k < 32; k += 4) {
+      for (int k = 0; k < C::KC; k += 4) {
         const double a0 = tab[ia], a1 = tab[ib];
         double b[8];
 #pragma unroll
@@ -277,7 +283,7 @@ __device__ __forceinline__ void big_dst_xT(const double* __restrict__ pv, const 
 }
 
 // DST along y in the normal mapping: out[j][i] = sum_l Sy[j][l] V[l][i].  Folded: K over l < HALF with
-// v_l +- v_{NP-2-l} (u for even unit rows = alpha odd, w for odd ones); mirror rows NP-34-l0 .. NP-2-l0.
+// v_l +- v_{NP-2-l} (u for even unit rows = alpha odd, w for odd ones); mirror rows NP-KC-2-l0 .. NP-2-l0.
 template <class C>
 __device__ __forceinline__ void big_dst_y(const double* __restrict__ pv, const double* __restrict__ tab, int L,
                                           double* stage, double (&acc)[8][4], const BigCtx& c, int ky_end,
@@ -288,7 +294,7 @@ __device__ __forceinline__ void big_dst_y(const double* __restrict__ pv, const d
     for (int e = 0; e < 4; ++e) acc[nf][e] = 0.0;
   double* st[2] = {stage, stage + C::STAGE};
   const int kend = fold ? C::HALF : ky_end;
-  const int nky = kend / 32 + ((kend & 31) ? 1 : 0);
+  const int nky = (kend + C::KC - 1) / C::KC;
   const int ja = big_row(c, 0) + 1, jb = big_row(c, 2) + 1;
   int ia = (ja * (c.tig + 1)) % L, ib = (jb * (c.tig + 1)) % L;
   const int sa = (4 * ja) % L, sb = (4 * jb) % L;
@@ -296,25 +302,25 @@ __device__ __forceinline__ void big_dst_y(const double* __restrict__ pv, const d
   const double sgn = w ? -1.0 : 1.0;
   const double sgn_last = (c.tig == 3) ? (w ? -1.0 : 0.0) : sgn;
   load_ychunk<C>(st[0], pv, 0, c.C0, c.tid);
-  if (fold) load_ychunk<C>(st[0] + C::CHUNK, pv, C::NP - 33, c.C0, c.tid);
+  if (fold) load_ychunk<C>(st[0] + C::CHUNK, pv, C::NP - C::KC - 1, c.C0, c.tid);
   cp_async_commit();
   for (int ch = 0; ch < nky; ++ch) {
     if (ch + 1 < nky) {
-      load_ychunk<C>(st[(ch + 1) & 1], pv, 32 * (ch + 1), c.C0, c.tid);
-      if (fold) load_ychunk<C>(st[(ch + 1) & 1] + C::CHUNK, pv, C::NP - 33 - 32 * (ch + 1), c.C0, c.tid);
+      load_ychunk<C>(st[(ch + 1) & 1], pv, C::KC * (ch + 1), c.C0, c.tid);
+      if (fold) load_ychunk<C>(st[(ch + 1) & 1] + C::CHUNK, pv, C::NP - C::KC - 1 - C::KC * (ch + 1), c.C0, c.tid);
     }
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
     const double* br = st[ch & 1] + (c.tig + 1) * C::YS + 16 * c.wc0 + c.gq + 8;
     if (fold) {
-      // partner row NP-2-l of l = l0 + ll sits at mirror row 32 - ll
-      const double* bm = st[ch & 1] + C::CHUNK + (32 - c.tig) * C::YS + 16 * c.wc0 + c.gq + 8;
-      const bool last_chunk = 32 * ch + 32 >= C::HALF;
+      // partner row NP-2-l of l = l0 + ll sits at mirror row KC - ll
+      const double* bm = st[ch & 1] + C::CHUNK + (C::KC - c.tig) * C::YS + 16 * c.wc0 + c.gq + 8;
+      const bool last_chunk = C::KC * ch + C::KC >= C::HALF;
 #pragma unroll 4
-      for (int l = 0; l < 32; l += 4) {
+      for (int l = 0; l < C::KC; l += 4) {
         const double a0 = tab[ia], a1 = tab[ib];
-        const double f = (last_chunk && l == 28) ? sgn_last : sgn;
+        const double f = (last_chunk && l == C::KC - 4) ? sgn_last : sgn;
         double b[8];
 #pragma unroll
         for (int nf = 0; nf < 8; ++nf) b[nf] = fma(f, bm[8 * nf - l * C::YS], br[l * C::YS + 8 * nf]);
@@ -327,7 +333,7 @@ __device__ __forceinline__ void big_dst_y(const double* __restrict__ pv, const d
       }
     } else {
 #pragma unroll 4
-      for (int l = 0; l < 32; l += 4) {
+      for (int l = 0; l < C::KC; l += 4) {
         const double a0 = tab[ia], a1 = tab[ib];
         double b[8];
 #pragma unroll
@@ -357,10 +363,46 @@ __device__ __forceinline__ double big_mass(const double* __restrict__ pv, int j,
   return cm * s;
 }
 
+// Synchronisation of the CTAs of one chain: cluster barriers and DSMEM (G <= 16), or a global-memory
+// barrier and global reduction slots (GSYNC: the CTAs are co-resident through a cooperative launch).
+template <class C>
+struct BigSync {
+  double* tred;                                 // cluster: this CTA's tile-partial slots (shared memory)
+  double* tred_peer[C::GSYNC ? 1 : C::G];       // cluster: the peers' slots
+  int* sched;                                   // chain index broadcast (shared memory / global)
+  int* sched_peer[C::GSYNC ? 1 : C::G];
+  unsigned* gbar;                               // GSYNC: this group's arrival counter (zeroed per launch)
+  double* gred;                                 // GSYNC: [2][4][G] tile partials
+  unsigned epoch;                               // GSYNC: barriers passed (thread 0)
+};
+
+template <class C>
+__device__ __forceinline__ void big_sync(BigSync<C>& sy) {
+  if constexpr (C::GSYNC) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      sy.epoch += 1;
+      __threadfence();  // this CTA's writes (ordered before by the CTA barrier) before the arrival
+      atomicAdd(sy.gbar, 1u);
+      const unsigned target = sy.epoch * (unsigned)C::G;
+      for (;;) {
+        unsigned v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(sy.gbar) : "memory");
+        if (v >= target) break;
+        __nanosleep(32);
+      }
+      __threadfence();
+    }
+    __syncthreads();
+  } else {
+    group_sync<C::G>();
+  }
+}
+
 // Deterministic group sum of NV values: unit (warp butterfly) -> tile (unit order) -> group (tile order).
 template <class C, int NV>
-__device__ __forceinline__ void big_reduce(double (&part)[NV][4], double* wred, double* tred,
-                                           double* const* tred_peer, int buf, const BigCtx& c, double (&out)[NV]) {
+__device__ __forceinline__ void big_reduce(double (&part)[NV][4], double* wred, BigSync<C>& sy, int buf,
+                                           const BigCtx& c, double (&out)[NV]) {
   // part[v][u]: this thread's partial for its warp strip's unit u (4 units per warp)
 #pragma unroll
   for (int v = 0; v < NV; ++v)
@@ -378,13 +420,25 @@ __device__ __forceinline__ void big_reduce(double (&part)[NV][4], double* wred, 
     for (int v = 0; v < NV; ++v) {
       double x = wred[v * 64 + c.lane] + wred[v * 64 + 32 + c.lane];
       x = warp_allsum(x);
-      if (c.lane < C::G) tred_peer[c.lane][buf * 4 * 16 + v * 16 + c.rank] = x;
+      if constexpr (C::GSYNC) {
+        if (c.lane == 0) sy.gred[(buf * 4 + v) * C::G + c.rank] = x;
+      } else {
+        if (c.lane < C::G) sy.tred_peer[c.lane][buf * 4 * 16 + v * 16 + c.rank] = x;
+      }
     }
   }
-  group_sync<C::G>();
+  big_sync<C>(sy);
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
-    double x = c.lane < C::G ? tred[buf * 4 * 16 + v * 16 + c.lane] : 0.0;
+    double x = 0.0;
+    if constexpr (C::GSYNC) {
+      const double* g = sy.gred + (buf * 4 + v) * C::G;
+#pragma unroll
+      for (int q = 0; q < C::G; q += 32)
+        if (q + c.lane < C::G) x += __ldcg(g + q + c.lane);
+    } else {
+      x = c.lane < C::G ? sy.tred[buf * 4 * 16 + v * 16 + c.lane] : 0.0;
+    }
     out[v] = warp_allsum(x);
   }
 }
@@ -406,20 +460,29 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
   c.warp = c.tid >> 5;
   c.gq = c.lane >> 2;
   c.tig = c.lane & 3;
-  c.rank = (int)cgx::this_cluster().block_rank();
+  if constexpr (C::GSYNC)
+    c.rank = blockIdx.x % C::G;
+  else
+    c.rank = (int)cgx::this_cluster().block_rank();
   c.R0 = 128 * (c.rank / C::TPR);
   c.C0 = 128 * (c.rank % C::TPR);
   c.wr = c.warp >> 1;
   c.wc0 = (c.warp & 1) * 4;
 
-  double* tred_peer[C::G];
-  int* sched_peer[C::G];
-  {
+  BigSync<C> sy;
+  sy.tred = tred;
+  sy.sched = sched;
+  sy.epoch = 0;
+  if constexpr (C::GSYNC) {
+    sy.gbar = P.gbar + (size_t)(blockIdx.x / C::G) * 32;
+    sy.gred = P.gbuf + (size_t)(blockIdx.x / C::G) * 1024;
+    sy.sched = reinterpret_cast<int*>(sy.gred + 8 * C::G);
+  } else {
     auto cl = cgx::this_cluster();
 #pragma unroll
     for (int q = 0; q < C::G; ++q) {
-      tred_peer[q] = cl.map_shared_rank(tred, q);
-      sched_peer[q] = cl.map_shared_rank(sched, q);
+      sy.tred_peer[q] = cl.map_shared_rank(tred, q);
+      sy.sched_peer[q] = cl.map_shared_rank(sched, q);
     }
   }
 
@@ -451,7 +514,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
   // zero the PV halos / padding of this cluster's vectors once (only interior points are ever written)
   for (size_t i = (size_t)c.rank * C::THREADS + c.tid; i < 2 * (size_t)C::PV; i += (size_t)C::G * C::THREADS)
     base[i] = 0.0;
-  group_sync<C::G>();
+  big_sync<C>(sy);
 
   int buf = 0;
   double acc[8][4];
@@ -461,12 +524,16 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
   for (;;) {
     if (c.rank == 0 && c.tid == 0) {
       const int ch = atomicAdd(P.chain_counter, 1);
+      if constexpr (C::GSYNC) {
+        sy.sched[0] = ch;
+      } else {
 #pragma unroll
-      for (int q = 0; q < C::G; ++q) sched_peer[q][0] = ch;
+        for (int q = 0; q < C::G; ++q) sy.sched_peer[q][0] = ch;
+      }
     }
-    group_sync<C::G>();
-    const int chain = sched[0];
-    group_sync<C::G>();
+    big_sync<C>(sy);
+    const int chain = C::GSYNC ? __ldcg(sy.sched) : sy.sched[0];
+    big_sync<C>(sy);
     if (chain >= W.nchains) break;
     const int n0 = W.first + chain * W.cstride;
     const int n1 = min(n0 + W.clen - 1, W.nmax);
@@ -487,7 +554,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
             const int j = big_row(c, e), i = big_col(c, nf, e);
             if (j < ny && i < nx) put_tile(pv0, j, i, __ldcg(src + j * nx + i));
           }
-          group_sync<C::G>();
+          big_sync<C>(sy);
         } else {
           __syncthreads();
         }
@@ -523,13 +590,13 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
       build_step_tables<C::NP, C::GL, C::THREADS>(gens, P.gens, s, cm, c.tid);  // M + s K from here on
       __syncthreads();
       if (W.x0_mode == 2) {
-        group_sync<C::G>();
+        big_sync<C>(sy);
         const double* x0 = W.d_x0 + (int64_t)n * W.x0_stride;
         RM_BIG_FOR {
           const int j = big_row(c, e), i = big_col(c, nf, e);
           if (j < ny && i < nx) put_tile(pv0, j, i, __ldcg(x0 + j * nx + i));
         }
-        group_sync<C::G>();
+        big_sync<C>(sy);
         big_matvec<C>(pv0, gens, stage, acc, c, kx_end, ky_end, P.merge);
         ++nmv;
         part[1][0] = part[1][1] = part[1][2] = part[1][3] = 0.0;
@@ -547,7 +614,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
         }
       }
       double tot[2];
-      big_reduce<C, 2>(part, wred, tred, tred_peer, buf, c, tot);
+      big_reduce<C, 2>(part, wred, sy, buf, c, tot);
       buf ^= 1;
       const double bnorm = sqrt(tot[0]);
       const double target = bnorm > 0.0 ? W.rel_tol * bnorm : W.rel_tol;
@@ -561,7 +628,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
             put_tile(pv0, j, i, Gr ? __ldcg(gu + gi) - __ldcg(Gr + gi) : __ldcg(gu + gi));
           }
         }
-        group_sync<C::G>();
+        big_sync<C>(sy);
         big_matvec<C>(pv0, gens, stage, acc, c, kx_end, ky_end, P.merge);
         ++nmv;
         double pg[1][4] = {{0, 0, 0, 0}};
@@ -573,7 +640,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
           pg[0][nf >> 1] += r * r;
         }
         double rg[1];
-        big_reduce<C, 1>(pg, wred, tred, tred_peer, buf, c, rg);
+        big_reduce<C, 1>(pg, wred, sy, buf, c, rg);
         buf ^= 1;
         if (rg[0] < tot[1]) {
           tot[1] = rg[0];
@@ -594,12 +661,12 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
       // z = P^-1 r (PRE) into acc; uses pv1 <- r, pv0 <- T1, pv1 <- T2 * dinv, pv0 <- T3
       auto apply_tau_big = [&]() {
         __syncthreads();
-        group_sync<C::G>();  // every CTA done reading pv0 / pv1
+        big_sync<C>(sy);  // every CTA done reading pv0 / pv1
         RM_BIG_FOR {
           const int j = big_row(c, e), i = big_col(c, nf, e);
           if (j < ny && i < nx) put_tile(pv1, j, i, __ldcg(rs + big_fidx(c, nf, e)));
         }
-        group_sync<C::G>();
+        big_sync<C>(sy);
 #pragma unroll 1
         for (int pass = 0; pass < 2; ++pass) {
           big_dst_xT<C>(pv1, tabx, Lx, stage, acc, c, kx_end, fold_x);
@@ -607,25 +674,25 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
             const int j = bigT_row(c, nf, e), i = bigT_col(c, e, fold_x);
             if (j < ny && i < nx) put_tile(pv0, j, i, acc[nf][e]);
           }
-          group_sync<C::G>();
+          big_sync<C>(sy);
           big_dst_y<C>(pv0, taby, Ly, stage, acc, c, ky_end, fold_y);
           if (pass == 1) break;
           RM_BIG_FOR {
             const int j = big_row(c, e), i = big_col(c, nf, e);
             if (j < ny && i < nx) put_tile(pv1, j, i, acc[nf][e] * __ldcg(ds + big_fidx(c, nf, e)));
           }
-          group_sync<C::G>();
+          big_sync<C>(sy);
         }
         ++npc;
       };
       auto set_direction_from = [&](bool use_z) {
         // p = z (PRE) or r into pv0 (after every CTA finished reading pv0)
-        group_sync<C::G>();
+        big_sync<C>(sy);
         RM_BIG_FOR {
           const int j = big_row(c, e), i = big_col(c, nf, e);
           if (j < ny && i < nx) put_tile(pv0, j, i, use_z ? acc[nf][e] : __ldcg(rs + big_fidx(c, nf, e)));
         }
-        group_sync<C::G>();
+        big_sync<C>(sy);
       };
 
       if (!done) {
@@ -634,7 +701,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
           double p1[1][4] = {{0, 0, 0, 0}};
           RM_BIG_FOR { p1[0][nf >> 1] += __ldcg(rs + big_fidx(c, nf, e)) * acc[nf][e]; }
           double rz[1];
-          big_reduce<C, 1>(p1, wred, tred, tred_peer, buf, c, rz);
+          big_reduce<C, 1>(p1, wred, sy, buf, c, rz);
           buf ^= 1;
           rr = rz[0];
           set_direction_from(true);
@@ -661,7 +728,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
           acc[nf][e] = ap;
         }
         double pap[1];
-        big_reduce<C, 1>(p1, wred, tred, tred_peer, buf, c, pap);
+        big_reduce<C, 1>(p1, wred, sy, buf, c, pap);
         buf ^= 1;
         if (!isfinite(pap[0]) || pap[0] <= 0.0) {
           fail = RM_CG_BREAKDOWN;
@@ -701,11 +768,11 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
         if constexpr (PRE) {
           apply_tau_big();
           RM_BIG_FOR { part2[1][nf >> 1] += __ldcg(rs + big_fidx(c, nf, e)) * acc[nf][e]; }
-          big_reduce<C, 2>(part2, wred, tred, tred_peer, buf, c, red2);
+          big_reduce<C, 2>(part2, wred, sy, buf, c, red2);
         } else {
           double p0[1][4] = {{part2[0][0], part2[0][1], part2[0][2], part2[0][3]}};
           double one[1];
-          big_reduce<C, 1>(p0, wred, tred, tred_peer, buf, c, one);
+          big_reduce<C, 1>(p0, wred, sy, buf, c, one);
           red2[0] = red2[1] = one[0];
         }
         buf ^= 1;
@@ -717,12 +784,12 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
           break;
         }
         if (res <= target) {
-          group_sync<C::G>();
+          big_sync<C>(sy);
           RM_BIG_FOR {
             const int j = big_row(c, e), i = big_col(c, nf, e);
             if (j < ny && i < nx) put_tile(pv0, j, i, xs[big_fidx(c, nf, e)]);
           }
-          group_sync<C::G>();
+          big_sync<C>(sy);
           big_matvec<C>(pv0, gens, stage, acc, c, kx_end, ky_end, P.merge);
           ++nmv;
           double pt[1][4] = {{0, 0, 0, 0}};
@@ -734,7 +801,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
             pt[0][nf >> 1] += rt * rt;
           }
           double tt[1];
-          big_reduce<C, 1>(pt, wred, tred, tred_peer, buf, c, tt);
+          big_reduce<C, 1>(pt, wred, sy, buf, c, tt);
           buf ^= 1;
           const double true_res = sqrt(tt[0]);
           if (true_res <= fmax(target, 10.0 * res)) {
@@ -754,7 +821,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
             double p3[1][4] = {{0, 0, 0, 0}};
             RM_BIG_FOR { p3[0][nf >> 1] += __ldcg(rs + big_fidx(c, nf, e)) * acc[nf][e]; }
             double rz[1];
-            big_reduce<C, 1>(p3, wred, tred, tred_peer, buf, c, rz);
+            big_reduce<C, 1>(p3, wred, sy, buf, c, rz);
             buf ^= 1;
             rr = rz[0];
             set_direction_from(true);
@@ -766,7 +833,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
         }
         const double beta = red2[1] / rr;
         rr = red2[1];
-        group_sync<C::G>();  // every CTA done reading pv0 (and the DST stages)
+        big_sync<C>(sy);  // every CTA done reading pv0 (and the DST stages)
         RM_BIG_FOR {
           const int j = big_row(c, e), i = big_col(c, nf, e);
           if (j < ny && i < nx) {
@@ -776,7 +843,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
             put_tile(pv0, j, i, zi + beta * pold);
           }
         }
-        group_sync<C::G>();
+        big_sync<C>(sy);
       }
 
       if (c.rank == 0 && c.tid == 0) {
@@ -791,7 +858,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
           P.fail_info[1] = (double)its;
           P.fail_info[2] = res;
         }
-        group_sync<C::G>();
+        big_sync<C>(sy);
         break;
       }
       // ---------------- MGRIT epilogue ----------------
@@ -800,7 +867,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
       const double* Gn = W.d_gadd ? W.d_gadd + (int64_t)n * W.gadd_stride : nullptr;
       const double* Sn = W.d_sub ? W.d_sub + (int64_t)n * W.sub_stride : nullptr;
       double* On = W.d_out ? W.d_out + (int64_t)oi * W.out_stride : nullptr;
-      group_sync<C::G>();  // every CTA done reading pv0 before it is overwritten with y
+      big_sync<C>(sy);  // every CTA done reading pv0 before it is overwritten with y
       double py[1][4] = {{0, 0, 0, 0}};
       RM_BIG_FOR {
         const int j = big_row(c, e), i = big_col(c, nf, e);
@@ -816,12 +883,12 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
       }
       if (W.d_norms) {
         double yy[1];
-        big_reduce<C, 1>(py, wred, tred, tred_peer, buf, c, yy);
+        big_reduce<C, 1>(py, wred, sy, buf, c, yy);
         buf ^= 1;
         if (c.rank == 0 && c.tid == 0) W.d_norms[oi] = yy[0];
       }
       in_tile = next_in_tile;
-      group_sync<C::G>();
+      big_sync<C>(sy);
     }
   }
 }
@@ -881,7 +948,7 @@ static cudaError_t launch_big_t(const ChainArgs& a, int max_clusters, cudaStream
   auto kern = a.sw.precond ? chain_big_kernel<C, true> : chain_big_kernel<C, false>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
   if (err != cudaSuccess) return err;
-  if (C::G > 8) {
+  if (C::G > 8 && !C::GSYNC) {
     err = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (err != cudaSuccess) return err;
   }
@@ -893,10 +960,16 @@ static cudaError_t launch_big_t(const ChainArgs& a, int max_clusters, cudaStream
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = C::G;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
+  if constexpr (C::GSYNC) {
+    if (!a.gbar || !a.gbuf) return cudaErrorInvalidValue;
+    attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs of a group co-resident (global barrier)
+    attr[0].val.cooperative = 1;
+  } else {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C::G;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+  }
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, a);
@@ -908,6 +981,15 @@ static cudaError_t max_clusters_big_t(int* out) {
   auto kern = chain_big_kernel<C, true>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
   if (err != cudaSuccess) return err;
+  if constexpr (C::GSYNC) {
+    int per_sm = 0, dev = 0, sms = 0;
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM);
+    if (err != cudaSuccess) return err;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    *out = per_sm * sms / C::G;
+    return cudaSuccess;
+  }
   if (C::G > 8) {
     err = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (err != cudaSuccess) return err;
@@ -926,7 +1008,7 @@ static cudaError_t max_clusters_big_t(int* out) {
   return cudaOccupancyMaxActiveClusters(out, kern, &cfg);
 }
 
-bool big_supported(int np) { return np == 256 || np == 512; }
+bool big_supported(int np) { return np == 256 || np == 512 || np == 1024; }
 
 int big_group(int np) { return (np / 128) * (np / 128); }
 
@@ -938,12 +1020,14 @@ size_t big_scratch_doubles_per_cluster(int np) {
 cudaError_t launch_big(int np, const ChainArgs& a, int max_clusters, cudaStream_t st) {
   if (np == 256) return launch_big_t<256>(a, max_clusters, st);
   if (np == 512) return launch_big_t<512>(a, max_clusters, st);
+  if (np == 1024) return launch_big_t<1024>(a, max_clusters, st);
   return cudaErrorInvalidValue;
 }
 
 cudaError_t big_max_clusters(int np, int* out) {
   if (np == 256) return max_clusters_big_t<256>(out);
   if (np == 512) return max_clusters_big_t<512>(out);
+  if (np == 1024) return max_clusters_big_t<1024>(out);
   return cudaErrorInvalidValue;
 }
 

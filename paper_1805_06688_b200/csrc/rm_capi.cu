@@ -54,6 +54,9 @@ struct rm_grid {
   int* d_fail = nullptr;
   double* d_fail_info = nullptr;
   long long* d_timing = nullptr;
+  unsigned* d_gbar = nullptr;  // NP = 1024: per-group barrier counters of the global-sync large-grid kernel
+  double* d_gbuf = nullptr;    //            and per-group reduction slots
+  int big_slots = 0;           // resident chain groups of the large-grid kernel
   double* d_dm = nullptr;  // tau preconditioner (rm_grid_set_tau)
   double* d_dk = nullptr;
   double* d_tab = nullptr;  // sine tables x then y
@@ -66,7 +69,7 @@ const char* rm_version(void) { return "riesz_mgrit_b200 0.1.0 (sm_100a, FP64 DMM
 
 const char* rm_last_error(void) { return g_err.c_str(); }
 
-int rm_max_order(void) { return 512; }
+int rm_max_order(void) { return 1024; }
 
 int rm_grid_create(int nx, int ny, const double* t1x_col, const double* t1x_row, const double* t2x_col,
                    const double* t2x_row, const double* t1y_col, const double* t1y_row, const double* t2y_col,
@@ -139,6 +142,7 @@ int rm_grid_create(int nx, int ny, const double* t1x_col, const double* t1x_row,
       return fail(RM_EUNSUP, "rm_grid_create: no resident cluster for the large-grid kernel");
     }
     for (int gi = 0; gi < 5; ++gi) g->max_clusters[gi] = kGroups[gi] == rm::big_group(np) ? n : 0;
+    g->big_slots = n;
     maxc = n;
     scratch_per_cluster = rm::big_scratch_doubles_per_cluster(np);
   }
@@ -163,7 +167,10 @@ int rm_grid_create(int nx, int ny, const double* t1x_col, const double* t1x_row,
       (e = cudaMemset(g->d_fail, 0, sizeof(int))) != cudaSuccess ||
       (e = cudaMalloc(&g->d_fail_info, 4 * sizeof(double))) != cudaSuccess ||
       (e = cudaMalloc(&g->d_timing, 16 * sizeof(long long))) != cudaSuccess ||
-      (e = cudaMemset(g->d_timing, 0, 16 * sizeof(long long))) != cudaSuccess) {
+      (e = cudaMemset(g->d_timing, 0, 16 * sizeof(long long))) != cudaSuccess ||
+      (rm::big_supported(np) && rm::big_group(np) > 16 &&
+       ((e = cudaMalloc(&g->d_gbar, sizeof(unsigned) * 32 * maxc)) != cudaSuccess ||
+        (e = cudaMalloc(&g->d_gbuf, sizeof(double) * 1024 * maxc)) != cudaSuccess))) {
     rm_grid_destroy(g);
     return cuda_fail(e, "rm_grid_create");
   }
@@ -179,6 +186,8 @@ int rm_grid_destroy(rm_grid* g) {
   cudaFree(g->d_fail);
   cudaFree(g->d_fail_info);
   cudaFree(g->d_timing);
+  cudaFree(g->d_gbar);
+  cudaFree(g->d_gbuf);
   cudaFree(g->d_dm);
   cudaFree(g->d_dk);
   cudaFree(g->d_tab);
@@ -264,8 +273,9 @@ int rm_sweep_run(rm_grid* g, const rm_sweep* sw, void* stream) {
   if (rm::big_supported(g->np)) {
     if (sw->group > 0 && sw->group != rm::big_group(g->np))
       return fail(RM_EUNSUP, "rm_sweep_run: the large-grid kernel uses a fixed cluster size");
-    const int gi_big = rm::big_group(g->np) == 4 ? 2 : 4;
     rm::ChainArgs a;
+    a.gbar = g->d_gbar;
+    a.gbuf = g->d_gbuf;
     a.sw = *sw;
     a.nx = g->nx;
     a.ny = g->ny;
@@ -283,7 +293,9 @@ int rm_sweep_run(rm_grid* g, const rm_sweep* sw, void* stream) {
     a.taby = g->d_tab ? g->d_tab + (2 * g->np + 8) : nullptr;
     cudaStream_t stb = (cudaStream_t)stream;
     RM_CUDA(cudaMemsetAsync(g->d_counter, 0, sizeof(int), stb), "rm_sweep_run: counter reset");
-    RM_CUDA(rm::launch_big(g->np, a, std::min(g->max_clusters[gi_big], g->scratch_clusters), stb),
+    if (g->d_gbar)
+      RM_CUDA(cudaMemsetAsync(g->d_gbar, 0, sizeof(unsigned) * 32 * g->big_slots, stb), "rm_sweep_run: barriers");
+    RM_CUDA(rm::launch_big(g->np, a, std::min(g->big_slots, g->scratch_clusters), stb),
             "rm_sweep_run: launch (large grid)");
     return RM_OK;
   }
@@ -298,6 +310,8 @@ int rm_sweep_run(rm_grid* g, const rm_sweep* sw, void* stream) {
   slots = std::min(slots, g->scratch_clusters);
   cudaStream_t st = (cudaStream_t)stream;
   rm::ChainArgs a;
+  a.gbar = nullptr;
+  a.gbuf = nullptr;
   a.sw = *sw;
   a.nx = g->nx;
   a.ny = g->ny;

@@ -24,6 +24,8 @@ struct ChainArgs {
   const double* dk;
   const double* tabx;  // sine tables sqrt(2/(n+1)) sin(pi m/(n+1)), m < 2(n+1) (device)
   const double* taby;
+  unsigned* gbar;      // large grids beyond the cluster limit: per-group barrier counters (32 words each)
+  double* gbuf;        // ... and per-group reduction / broadcast slots (1024 doubles each)
 };
 
 struct ApplyArgs {
@@ -53,7 +55,7 @@ cudaError_t launch_apply(int np, const ApplyArgs& a, int batch, cudaStream_t st)
 cudaError_t launch_pcg64(const PcgArgs& a, cudaStream_t st);
 cudaError_t launch_correct(int ndof, int nc, int m, double* u, int64_t us, const double* uc, int64_t ucs,
                            cudaStream_t st);
-bool big_supported(int np);
+bool big_supported(int np);  // 256, 512 (clusters), 1024 (global-memory group barrier)
 int big_group(int np);
 size_t big_scratch_doubles_per_cluster(int np);
 cudaError_t launch_big(int np, const ChainArgs& a, int max_clusters, cudaStream_t st);

@@ -30,7 +30,8 @@ def dst_matrix(n: int) -> np.ndarray:
 
 
 def _sts(S: np.ndarray, T: np.ndarray) -> np.ndarray:
-    return np.einsum("ij,jk,ki->i", S, T, S)
+    """diag(S T S) through one GEMM (S symmetric): O(n^3) on the BLAS, 1023^2 grids in well under a second."""
+    return np.einsum("ij,ij->i", S @ T, S)
 
 
 def _toeplitz(col, row):
