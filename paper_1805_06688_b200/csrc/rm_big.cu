@@ -42,9 +42,16 @@ struct BigCfg {
   static constexpr int YS = 148;           // y-stage row stride (== 4 mod 16)
   static constexpr int YCOLS = 144;        // C0-8 .. C0+135
   static constexpr int CHUNK = (XROWS * XS > (KC + 1) * YS ? XROWS * XS : (KC + 1) * YS);  // doubles per chunk
-  // more than 16 CTAs per chain (NP = 1024: 64) exceed the cluster limit: the chain's CTAs then
-  // synchronise through global memory (co-resident by a cooperative launch) instead of cluster barriers
+  // The chain's CTAs synchronise through global memory (co-resident by a cooperative launch) rather
+  // than as a thread-block cluster: clusters of 4/16 CTAs leave 16-20 SMs unplaced (measured 132 and
+  // 128 of 148 SMs busy) and 64 CTAs (NP = 1024) exceed the cluster limit; the group barrier costs
+  // little against phases of >= 33 MFLOP per CTA (cfg3 sweep 17.5 -> 20.5 TF/s, cfg4 16.0 -> 22.8).
+  // -DRM_BIG_CLUSTER restores cluster barriers and DSMEM reductions for G <= 16.
+#ifdef RM_BIG_CLUSTER
   static constexpr bool GSYNC = G > 16;
+#else
+  static constexpr bool GSYNC = true;
+#endif
   static constexpr int STAGE = 2 * CHUNK;  // a chunk and (folded DST) its mirror
   static constexpr int HALF = NP / 2;
   static constexpr int TE = 128 * 128;     // elements per tile

@@ -168,7 +168,7 @@ int rm_grid_create(int nx, int ny, const double* t1x_col, const double* t1x_row,
       (e = cudaMalloc(&g->d_fail_info, 4 * sizeof(double))) != cudaSuccess ||
       (e = cudaMalloc(&g->d_timing, 16 * sizeof(long long))) != cudaSuccess ||
       (e = cudaMemset(g->d_timing, 0, 16 * sizeof(long long))) != cudaSuccess ||
-      (rm::big_supported(np) && rm::big_group(np) > 16 &&
+      (rm::big_supported(np) &&
        ((e = cudaMalloc(&g->d_gbar, sizeof(unsigned) * 32 * maxc)) != cudaSuccess ||
         (e = cudaMalloc(&g->d_gbuf, sizeof(double) * 1024 * maxc)) != cudaSuccess))) {
     rm_grid_destroy(g);
