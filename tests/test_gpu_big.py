@@ -79,3 +79,26 @@ def test_big_mgrit_matches_reference(golden, tag, name, nt, pre, fixture):
         assert rel(U[n], R[k]) <= 1e-10
     norms = np.linalg.norm(U, axis=1)
     assert np.allclose(norms, g[f"{tag}_norms"], rtol=1e-10, atol=0)
+
+
+@pytest.mark.parametrize("pre", ["none", "tau"])
+def test_big_sequential_and_residual_match_oracle(pre):
+    """Large-grid kernel through sequential_solve (rhs F_n + explicit U[n-1], warm start) and
+    spacetime_residual (given iterate, x0_mode 2): config-4 structure (graded mesh, f = e^-t g) on 255^2."""
+    from paper_1805_06688_b200.stepper import sequential_solve, spacetime_residual
+
+    case = make_case("cfg4", M=256, Nt=6)
+    spec = ProblemSpec(**case.problem_kwargs())
+    prob = O.Problem(O.Grid(256, 256), spec.tmesh.points, case.kx, case.ky, case.beta, case.gamma, spec.source,
+                     spec.initial)
+    st = O.Stepper(prob, rel_tol=1e-12)
+    R = O.sequential(prob, st)
+    disc = Discretization(spec, cg_opts=CgOptions(rel_tol=1e-12, preconditioner=pre))
+    U = sequential_solve(spec, disc)
+    for n in range(R.shape[0]):
+        assert rel(U[n], R[n]) <= 1e-10
+    Up = R + 1e-3 * np.random.default_rng(5).standard_normal(R.shape)
+    norms, tot = spacetime_residual(spec, Up, disc)
+    want, wtot = O.spacetime_residual(prob, Up, st)
+    assert np.allclose(norms, want, rtol=1e-8, atol=1e-14)
+    assert tot == pytest.approx(wtot, rel=1e-8)
