@@ -55,7 +55,8 @@ struct BigCfg {
   static constexpr int STAGE = 2 * CHUNK;  // a chunk and (folded DST) its mirror
   static constexpr int HALF = NP / 2;
   static constexpr int TE = 128 * 128;     // elements per tile
-  static constexpr size_t SMEM = sizeof(double) * (6 * GL + 2 * GL + 2 * STAGE + 4 * 64 + 2 * 4 * 16) + 64;
+  static constexpr int TL = (GL + GL / 8 + 3) & ~1;  // padded sine table (tab_idx), even length
+  static constexpr size_t SMEM = sizeof(double) * (6 * GL + 2 * TL + 2 * STAGE + 4 * 64 + 2 * 4 * 16) + 64;
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
@@ -258,7 +259,7 @@ __device__ __forceinline__ void big_dst_xT(const double* __restrict__ pv, const 
       const bool last_chunk = C::KC * ch + C::KC >= C::HALF;
 #pragma unroll 4
       for (int k = 0; k < C::KC; k += 4) {
-        const double a0 = tab[ia], a1 = tab[ib];
+        const double a0 = tab[tab_idx(ia)], a1 = tab[tab_idx(ib)];
         const double f = (last_chunk && k == C::KC - 4) ? sgn_last : sgn;
         double b[8];
 #pragma unroll
@@ -273,7 +274,7 @@ __device__ __forceinline__ void big_dst_xT(const double* __restrict__ pv, const 
     } else {
 #pragma unroll 4
       for (int k = 0; k < C::KC; k += 4) {
-        const double a0 = tab[ia], a1 = tab[ib];
+        const double a0 = tab[tab_idx(ia)], a1 = tab[tab_idx(ib)];
         double b[8];
 #pragma unroll
         for (int nf = 0; nf < 8; ++nf) b[nf] = br[8 * nf * C::XS + k];
@@ -326,7 +327,7 @@ __device__ __forceinline__ void big_dst_y(const double* __restrict__ pv, const d
       const bool last_chunk = C::KC * ch + C::KC >= C::HALF;
 #pragma unroll 4
       for (int l = 0; l < C::KC; l += 4) {
-        const double a0 = tab[ia], a1 = tab[ib];
+        const double a0 = tab[tab_idx(ia)], a1 = tab[tab_idx(ib)];
         const double f = (last_chunk && l == C::KC - 4) ? sgn_last : sgn;
         double b[8];
 #pragma unroll
@@ -341,7 +342,7 @@ __device__ __forceinline__ void big_dst_y(const double* __restrict__ pv, const d
     } else {
 #pragma unroll 4
       for (int l = 0; l < C::KC; l += 4) {
-        const double a0 = tab[ia], a1 = tab[ib];
+        const double a0 = tab[tab_idx(ia)], a1 = tab[tab_idx(ib)];
         double b[8];
 #pragma unroll
         for (int nf = 0; nf < 8; ++nf) b[nf] = br[l * C::YS + 8 * nf];
@@ -455,8 +456,8 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
   extern __shared__ __align__(16) double smem[];
   double* gens = smem;
   double* tabx = gens + 6 * C::GL;
-  double* taby = tabx + C::GL;
-  double* stage = taby + C::GL;
+  double* taby = tabx + C::TL;
+  double* stage = taby + C::TL;
   double* wred = stage + 2 * C::STAGE;  // 4 values x 64 units
   double* tred = wred + 4 * 64;         // 2 buffers x 4 values x 16 tiles
   int* sched = reinterpret_cast<int*>(tred + 2 * 4 * 16);
@@ -503,8 +504,8 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
   const bool fold_x = nx == C::NP - 1, fold_y = ny == C::NP - 1;  // even/odd folded DST stages
 
   if constexpr (PRE) {
-    for (int i = c.tid; i < Lx; i += C::THREADS) tabx[i] = P.tabx[i];
-    for (int i = c.tid; i < Ly; i += C::THREADS) taby[i] = P.taby[i];
+    for (int i = c.tid; i < Lx; i += C::THREADS) tabx[tab_idx(i)] = P.tabx[i];
+    for (int i = c.tid; i < Ly; i += C::THREADS) taby[tab_idx(i)] = P.taby[i];
   }
 
   // per-cluster scratch: two PV vectors, then per-CTA fragment-native vectors

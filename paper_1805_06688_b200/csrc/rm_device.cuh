@@ -56,7 +56,7 @@ struct Cfg {
   static constexpr int GL = 2 * NP + 8;  // generator table length
   static constexpr int RED = 2 * 4 * U;  // two reduction buffers of up to 4 values per unit
   static constexpr int XS = CU * 256;    // CG iterate of this CTA's units (shared-memory resident)
-  static constexpr int ST = 2 * NP + 8;  // sine table length (>= 2(n+1))
+  static constexpr int ST = (2 * NP + 8 + (2 * NP + 8) / 8 + 3) & ~1;  // padded sine table (tab_idx), even length
   static constexpr size_t SMEM = sizeof(double) * (VT + 6 * GL + RED + XS + 2 * ST) + 64;
   static constexpr size_t APPLY_SMEM = sizeof(double) * (VT + 6 * GL);
   // Row permutation: unit row ur holds rows 32*(ur/2) + (ur%2) + 2t, t < 16 (one parity inside a
@@ -157,6 +157,22 @@ __device__ __forceinline__ void matvec_yseg(const double* __restrict__ Vt, const
   }
 }
 
+// Row of transposed-stage fragment column r (0..15) of unit row u: when the CTA's own rows form one
+// contiguous band (even number of own unit rows), the x-stage (fold along columns) may use natural
+// row order -- rows 2 apart would put 4 lanes on one shared-memory bank; else the unit's rows.
+template <class C>
+__device__ __forceinline__ int trow(int u, int r) {
+  constexpr bool NATURAL = (C::G <= C::UR) && (!C::FOLD || (C::CR % 2 == 0));
+  if constexpr (NATURAL)
+    return 16 * u + r;
+  else
+    return prow<C>(u, r);
+}
+
+// Sine tables live in shared memory with one pad slot per 8 entries: the DST A operand reads entry
+// (alpha*kappa) mod 2(n+1) per lane, which without padding puts up to 8 lanes on one bank.
+__device__ __forceinline__ int tab_idx(int m) { return m + (m >> 3); }
+
 // acc[mr][nf][e] = X + Y over the warp's units (see file comment).
 // merge bit 0 (x) / bit 1 (y): the off-diagonal Toeplitz block T2 satisfies t2(d) = t2(-1-d)
 // (its first column is its first row shifted by one, assembly.py:239-249), hence
@@ -246,7 +262,7 @@ __device__ __forceinline__ void dst_y(const double* __restrict__ Vt, const doubl
     const double* bp = br + (C::NP - 2 - 2 * tig) * C::S;  // row NP-2-l for row l = l0 + tig
 #pragma unroll 4
     for (int l0 = 0; l0 < C::HALF; l0 += 4) {
-      const double a0 = tab[ia], a1 = tab[ib];
+      const double a0 = tab[tab_idx(ia)], a1 = tab[tab_idx(ib)];
       const double f = l0 == C::HALF - 4 ? sgn_last : sgn;
       double b[C::NF];
 #pragma unroll
@@ -262,7 +278,7 @@ __device__ __forceinline__ void dst_y(const double* __restrict__ Vt, const doubl
   }
 #pragma unroll 4
   for (int l0 = 0; l0 < k_end; l0 += 4) {
-    const double a0 = tab[ia], a1 = tab[ib];
+    const double a0 = tab[tab_idx(ia)], a1 = tab[tab_idx(ib)];
     double b[C::NF];
 #pragma unroll
     for (int nf = 0; nf < C::NF; ++nf) b[nf] = br[l0 * C::S + 8 * nf];
@@ -297,7 +313,7 @@ __device__ __forceinline__ void dst_xT(const double* __restrict__ Vt, const doub
   const int sa = (4 * xa) % L, sb = (4 * xb) % L;
   const double* br[C::NF];
 #pragma unroll
-  for (int nf = 0; nf < C::NF; ++nf) br[nf] = Vt + vt_idx<C>(prow<C>(tn + (nf >> 1), 8 * (nf & 1) + gq), tig);
+  for (int nf = 0; nf < C::NF; ++nf) br[nf] = Vt + vt_idx<C>(trow<C>(tn + (nf >> 1), 8 * (nf & 1) + gq), tig);
   if (fold) {
     const bool w = 16 * tm >= C::HALF;
     const double sgn = w ? -1.0 : 1.0;
@@ -305,7 +321,7 @@ __device__ __forceinline__ void dst_xT(const double* __restrict__ Vt, const doub
     const int off = C::NP - 2 - 2 * tig;  // column NP-2-k for column k = k0 + tig
 #pragma unroll 4
     for (int k0 = 0; k0 < C::HALF; k0 += 4) {
-      const double a0 = tab[ia], a1 = tab[ib];
+      const double a0 = tab[tab_idx(ia)], a1 = tab[tab_idx(ib)];
       const double f = k0 == C::HALF - 4 ? sgn_last : sgn;
       double b[C::NF];
 #pragma unroll
@@ -321,7 +337,7 @@ __device__ __forceinline__ void dst_xT(const double* __restrict__ Vt, const doub
   }
 #pragma unroll 4
   for (int k0 = 0; k0 < k_end; k0 += 4) {
-    const double a0 = tab[ia], a1 = tab[ib];
+    const double a0 = tab[tab_idx(ia)], a1 = tab[tab_idx(ib)];
     double b[C::NF];
 #pragma unroll
     for (int nf = 0; nf < C::NF; ++nf) b[nf] = br[nf][k0];

@@ -136,7 +136,7 @@ __device__ __forceinline__ int elem_xidx(const Ctx<C>& c, int mr, int nf, int e)
 // element (row j, col i) held by (nf, e) of the transposed DST-x stage
 template <class C>
 __device__ __forceinline__ int elemT_row(const Ctx<C>& c, int nf, int e) {
-  return prow<C>(c.tn + (nf >> 1), 8 * (nf & 1) + 2 * c.tig + (e & 1));
+  return trow<C>(c.tn + (nf >> 1), 8 * (nf & 1) + 2 * c.tig + (e & 1));
 }
 
 
@@ -296,8 +296,8 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
 
   for (int i = c.tid; i < C::VT; i += C::THREADS) Vt[i] = 0.0;
   if constexpr (PRE) {
-    for (int i = c.tid; i < Lx; i += C::THREADS) sm.tabx[i] = P.tabx[i];
-    for (int i = c.tid; i < Ly; i += C::THREADS) sm.taby[i] = P.taby[i];
+    for (int i = c.tid; i < Lx; i += C::THREADS) sm.tabx[tab_idx(i)] = P.tabx[i];
+    for (int i = c.tid; i < Ly; i += C::THREADS) sm.taby[tab_idx(i)] = P.taby[i];
   }
   Bcast<C> bc;
   bcast_setup<C>(bc, Vt, mbar, c.tid);
