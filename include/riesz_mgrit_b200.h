@@ -97,6 +97,7 @@ RM_API int rm_apply_batched(const rm_grid* grid, int which, int batch, const dou
  * then forms y_n = [d_gadd ? G_n + x : x] - [d_sub ? S_n : 0] and stores
  *     d_out + (n / out_div) * out_stride  <- y_n            (if d_out)
  *     d_norms[n / out_div]                <- y_n . y_n      (if d_norms)
+ *     d_keep + (n / out_div) * keep_stride <- y_n + S_n      (if d_keep)
  * The input of the first step of a chain is d_src + (n-1)*src_stride; later
  * steps take the previous step's output (requires d_out and out_div == 1).
  * Replaces: f_relax / c_relax (mgrit.py:147-165), restrict_residual (:174-182),
@@ -140,6 +141,10 @@ typedef struct rm_sweep {
      is about to overwrite).  NULL: off. */
   const double* d_guess;
   int64_t guess_stride;
+  /* optional: also write the step result before the subtraction, [G_n +] x, to d_keep[n / out_div]
+     (the residual sweep keeps the C-relaxation values the next cycle would recompute).  NULL: off. */
+  double* d_keep;
+  int64_t keep_stride;
 } rm_sweep;
 
 RM_API int rm_sweep_run(rm_grid* grid, const rm_sweep* sweep, void* stream);

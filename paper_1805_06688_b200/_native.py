@@ -43,6 +43,7 @@ class Sweep(C.Structure):
         ("precond", C.c_int),
         ("d_guess", C.c_void_p),
         ("guess_stride", C.c_int64),
+        ("d_keep", C.c_void_p), ("keep_stride", C.c_int64),
     ]
 
 

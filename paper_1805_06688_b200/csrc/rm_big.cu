@@ -875,6 +875,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
       const double* Gn = W.d_gadd ? W.d_gadd + (int64_t)n * W.gadd_stride : nullptr;
       const double* Sn = W.d_sub ? W.d_sub + (int64_t)n * W.sub_stride : nullptr;
       double* On = W.d_out ? W.d_out + (int64_t)oi * W.out_stride : nullptr;
+      double* Kn = W.d_keep ? W.d_keep + (int64_t)oi * W.keep_stride : nullptr;
       big_sync<C>(sy);  // every CTA done reading pv0 before it is overwritten with y
       double py[1][4] = {{0, 0, 0, 0}};
       RM_BIG_FOR {
@@ -883,6 +884,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
           const int gi = j * nx + i;
           double y = xs[big_fidx(c, nf, e)];
           if (Gn) y = __ldcg(Gn + gi) + y;
+          if (Kn) Kn[gi] = y;
           if (Sn) y = y - __ldcg(Sn + gi);
           if (On) On[gi] = y;
           if (next_in_tile) put_tile(pv0, j, i, y);

@@ -653,6 +653,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
       const double* Gn = W.d_gadd ? W.d_gadd + (int64_t)n * W.gadd_stride : nullptr;
       const double* Sn = W.d_sub ? W.d_sub + (int64_t)n * W.sub_stride : nullptr;
       double* On = W.d_out ? W.d_out + (int64_t)oi * W.out_stride : nullptr;
+      double* Kn = W.d_keep ? W.d_keep + (int64_t)oi * W.keep_stride : nullptr;
       double p1[1][C::WR][C::WC];
       zero_part<C>(p1[0]);
       RM_FOR_ELEM {
@@ -661,6 +662,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           const int gi = j * nx + i;
           double y = xs[elem_xidx<C>(c, mr, nf, e)];
           if (Gn) y = __ldcg(Gn + gi) + y;
+          if (Kn) Kn[gi] = y;
           if (Sn) y = y - __ldcg(Sn + gi);
           if (On) On[gi] = y;
           if (next_in_tile) Vt[vt_idx<C>(j, i)] = y;

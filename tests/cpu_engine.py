@@ -30,7 +30,7 @@ class CpuEngine:
 
     def sweep(self, *, nchains, first, cstride, clen, nmax, dt, counters, rel_tol, src=None, explicit=True,
               x0_mode=1, x0=None, f=None, f_stride=0, fscale=None, gadd=None, sub=None, out=None, out_div=1,
-              norms=None, max_iter=None, group=0, row=None, tag="", precond="none", guess=None):
+              norms=None, max_iter=None, group=0, row=None, tag="", precond="none", guess=None, keep=None):
         self.launches += 1
         for c in range(nchains):
             n0 = first + c * cstride
@@ -58,6 +58,8 @@ class CpuEngine:
                 y = x
                 if gadd is not None:
                     y = _row(gadd, n).numpy() + y
+                if keep is not None:
+                    _row(keep, n // out_div).copy_(torch.from_numpy(y))
                 if sub is not None:
                     y = y - _row(sub, n).numpy()
                 if out is not None:

@@ -101,3 +101,26 @@ def test_distributed_trace_bitwise_equal(world, tags):
         assert solves == tr1.spatial_solves, (tag, rank)
         assert cgits == tr1.cg_iterations, (tag, rank)
         assert np.array_equal(U, U1), (tag, rank)
+
+
+OPTS["noskip_fcf"] = dict(m=4, halt_tol=1e-10, cg_rel_tol=1e-12, skip_first_down=False, cg_preconditioner="none")
+
+
+@pytest.mark.parametrize("tag", ["multi", "two", "noskip_f", "noskip_fcf"])
+def test_single_rank_driver_matches_oracle(tag):
+    """The host driver's work elision (residual F-relaxation done in place, the C-relaxation taken from
+    the values the residual sweep kept) reproduces the reference's trace: same residual norms, spatial
+    solve and CG iteration counts as the oracle's straight restatement of mgrit.py:200-322."""
+    from oracle import riesz_oracle as O
+
+    U, tr = _run(tag, False)
+    spec = _spec()
+    prob = O.Problem(O.Grid(spec.grid.mx, spec.grid.my), spec.tmesh.points, spec.kx, spec.ky, spec.beta, spec.gamma,
+                     spec.source, spec.initial)
+    o = {k: v for k, v in OPTS[tag].items() if k != "cg_preconditioner"}
+    R, rtr = O.mgrit_solve(prob, O.Options(**o))
+    assert tr.iterations == rtr.iterations
+    assert tr.spatial_solves == rtr.spatial_solves
+    assert tr.cg_iterations == rtr.cg_iterations
+    np.testing.assert_allclose(tr.residual_norms, rtr.residual_norms, rtol=1e-9)
+    np.testing.assert_allclose(U, R, rtol=0, atol=1e-13 * np.abs(R).max())
