@@ -376,7 +376,7 @@ def main():
     ap.add_argument("--nt", type=int, default=None)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--precond", choices=["tau", "none"], default="tau",
+    ap.add_argument("--precond", choices=["tau", "tau64", "none"], default="tau",
                     help="inner CG: tau-preconditioned (default) or the reference's plain CG")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -113,7 +113,8 @@ RM_API int rm_apply_batched(const rm_grid* grid, int which, int batch, const dou
 typedef struct rm_sweep {
   int nchains, first, cstride, clen, nmax;
   int explicit_rhs; /* 0/1 */
-  int x0_mode;      /* 0 zero, 1 warm (in_n), 2 d_x0 */
+  int x0_mode;      /* 0 zero, 1 warm (in_n), 2 d_x0; 3 = preconditioner probe: x = P^-1 b_n, no CG
+                       (needs precond > 0; grids up to 127^2) */
   int out_div;
   const double* d_dt;
   const double* d_src;
@@ -135,7 +136,9 @@ typedef struct rm_sweep {
   unsigned long long* d_counters;
   int group;   /* CTAs per chain (cluster size); 0 = library choice */
   int precond; /* 0: plain CG (the reference algorithm); 1: tau-preconditioned CG (needs
-                  rm_grid_set_tau); both stop on ||b - A x|| <= rel_tol ||b|| */
+                  rm_grid_set_tau), DST stages in FP64; 2: the same preconditioner with its DST stages
+                  on FP16 tensor cores (scaled, FP32 accumulation; square grids up to 127^2, others run 1);
+                  all stop on ||b - A x|| <= rel_tol ||b|| in FP64 */
   /* optional second starting guess x0' = guess_n - G_n (G_n only when d_gadd): the solve starts
      from whichever of x0, x0' has the smaller initial residual (e.g. the iterate value this step
      is about to overwrite).  NULL: off. */

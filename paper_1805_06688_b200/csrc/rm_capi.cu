@@ -1,8 +1,10 @@
 // extern "C" boundary of the B200 hot path (declared in include/riesz_mgrit_b200.h).
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <string.h>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -60,6 +62,8 @@ struct rm_grid {
   double* d_dm = nullptr;  // tau preconditioner (rm_grid_set_tau)
   double* d_dk = nullptr;
   double* d_tab = nullptr;  // sine tables x then y
+  uint16_t* d_dst16 = nullptr;  // FP16 DST-I matrix [np][np+8] (chain kernel, precond 2, nx == ny)
+  double lp_dmin = 0.0, lp_kmin = 0.0;  // min over the grid of the tau diagonals dm, dk
   int max_clusters[5] = {0, 0, 0, 0, 0};
 };
 
@@ -191,6 +195,7 @@ int rm_grid_destroy(rm_grid* g) {
   cudaFree(g->d_dm);
   cudaFree(g->d_dk);
   cudaFree(g->d_tab);
+  cudaFree(g->d_dst16);
   delete g;
   return RM_OK;
 }
@@ -263,13 +268,16 @@ int rm_sweep_run(rm_grid* g, const rm_sweep* sw, void* stream) {
   if (sw->clen < 1 || sw->first < 1 || sw->nmax < sw->first) return fail(RM_EINVAL, "rm_sweep_run: bad chain shape");
   if (sw->out_div < 1) return fail(RM_EINVAL, "rm_sweep_run: out_div must be >= 1");
   if ((sw->explicit_rhs || sw->x0_mode == 1) && !sw->d_src) return fail(RM_EINVAL, "rm_sweep_run: d_src required");
-  if (sw->x0_mode < 0 || sw->x0_mode > 2) return fail(RM_EINVAL, "rm_sweep_run: x0_mode must be 0, 1 or 2");
+  if (sw->x0_mode < 0 || sw->x0_mode > 3) return fail(RM_EINVAL, "rm_sweep_run: x0_mode must be 0..3");
+  if (sw->x0_mode == 3 && (!sw->precond || rm::big_supported(g->np)))
+    return fail(RM_EUNSUP, "rm_sweep_run: x0_mode 3 (preconditioner probe) needs precond > 0 and a grid up to 127^2");
   if (sw->x0_mode == 2 && !sw->d_x0) return fail(RM_EINVAL, "rm_sweep_run: d_x0 required for x0_mode 2");
   if (sw->clen > 1 && (!sw->d_out || sw->out_div != 1))
     return fail(RM_EINVAL, "rm_sweep_run: chains longer than one step need d_out with out_div == 1");
   if (!sw->d_counters) return fail(RM_EINVAL, "rm_sweep_run: d_counters is required");
   if (!(sw->rel_tol > 0)) return fail(RM_EINVAL, "relative tolerance must be positive");
-  if (sw->precond && !g->d_dm) return fail(RM_EINVAL, "rm_sweep_run: precond=1 needs rm_grid_set_tau first");
+  if (sw->precond < 0 || sw->precond > 2) return fail(RM_EINVAL, "rm_sweep_run: precond must be 0, 1 or 2");
+  if (sw->precond && !g->d_dm) return fail(RM_EINVAL, "rm_sweep_run: precond needs rm_grid_set_tau first");
   if (rm::big_supported(g->np)) {
     if (sw->group > 0 && sw->group != rm::big_group(g->np))
       return fail(RM_EUNSUP, "rm_sweep_run: the large-grid kernel uses a fixed cluster size");
@@ -277,6 +285,9 @@ int rm_sweep_run(rm_grid* g, const rm_sweep* sw, void* stream) {
     a.gbar = g->d_gbar;
     a.gbuf = g->d_gbuf;
     a.sw = *sw;
+    if (a.sw.precond == 2) a.sw.precond = 1;  // the large-grid kernel runs its DST stages in FP64 (for now)
+    a.dst16 = nullptr;
+    a.lp_dmin = a.lp_kmin = 0.0;
     a.nx = g->nx;
     a.ny = g->ny;
     a.cm = g->cm;
@@ -313,6 +324,10 @@ int rm_sweep_run(rm_grid* g, const rm_sweep* sw, void* stream) {
   a.gbar = nullptr;
   a.gbuf = nullptr;
   a.sw = *sw;
+  a.dst16 = g->d_dst16;
+  a.lp_dmin = g->lp_dmin;
+  a.lp_kmin = g->lp_kmin;
+  if (a.sw.precond == 2 && !g->d_dst16) a.sw.precond = 1;  // nx != ny: DST stages in FP64
   a.nx = g->nx;
   a.ny = g->ny;
   a.cm = g->cm;
@@ -354,6 +369,27 @@ int rm_grid_set_tau(rm_grid* g, const double* dm, const double* dk) {
   RM_CUDA(cudaMemcpy(g->d_dm, dm, n * sizeof(double), cudaMemcpyHostToDevice), "rm_grid_set_tau");
   RM_CUDA(cudaMemcpy(g->d_dk, dk, n * sizeof(double), cudaMemcpyHostToDevice), "rm_grid_set_tau");
   RM_CUDA(cudaMemcpy(g->d_tab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice), "rm_grid_set_tau");
+  g->lp_dmin = dm[0];
+  g->lp_kmin = dk[0];
+  for (size_t i = 1; i < n; ++i) {
+    g->lp_dmin = std::min(g->lp_dmin, dm[i]);
+    g->lp_kmin = std::min(g->lp_kmin, dk[i]);
+  }
+  if (!rm::big_supported(np) && g->nx == g->ny) {
+    // FP16 DST-I matrix for the low-precision stages: row alpha-1, column kappa-1, zero beyond n
+    // (rm_device.cuh Lp); |S| <= sqrt(2/(n+1)) and every nonzero entry is an FP16 normal number
+    const int sh = np + 8, nn = g->nx;
+    std::vector<uint16_t> h((size_t)np * sh, 0);
+    const double c = sqrt(2.0 / (nn + 1));
+    for (int a = 0; a < nn; ++a)
+      for (int b = 0; b < nn; ++b) {
+        const double v = c * sin(M_PI * (double)((a + 1) * (b + 1) % (2 * (nn + 1))) / (double)(nn + 1));
+        h[(size_t)a * sh + b] = __half_as_ushort(__float2half_rn((float)v));
+      }
+    if (!g->d_dst16 && (e = cudaMalloc(&g->d_dst16, h.size() * sizeof(uint16_t))) != cudaSuccess)
+      return cuda_fail(e, "rm_grid_set_tau");
+    RM_CUDA(cudaMemcpy(g->d_dst16, h.data(), h.size() * sizeof(uint16_t), cudaMemcpyHostToDevice), "rm_grid_set_tau");
+  }
   return RM_OK;
 }
 

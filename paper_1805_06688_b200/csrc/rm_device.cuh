@@ -57,7 +57,7 @@ struct Cfg {
   static constexpr int RED = 2 * 4 * U;  // two reduction buffers of up to 4 values per unit
   static constexpr int XS = CU * 256;    // CG iterate of this CTA's units (shared-memory resident)
   static constexpr int ST = (2 * NP + 8 + (2 * NP + 8) / 8 + 3) & ~1;  // padded sine table (tab_idx), even length
-  static constexpr size_t SMEM = sizeof(double) * (VT + 6 * GL + RED + XS + 2 * ST) + 64;
+  static constexpr size_t SMEM = sizeof(double) * (VT + 6 * GL + RED + XS + 2 * ST) + 64 + 8 * 64;  // + mbarriers, schedule slot, |r| maxima
   static constexpr size_t APPLY_SMEM = sizeof(double) * (VT + 6 * GL);
   // Row permutation: unit row ur holds rows 32*(ur/2) + (ur%2) + 2t, t < 16 (one parity inside a
   // 32-row block) so that the DST even/odd folding gives every MMA fragment a single K operand.
@@ -400,6 +400,127 @@ __device__ __forceinline__ void group_sync() {
 }
 
 // ----------------------------------------------------------------------------
+// Low-precision DST stages of the tau preconditioner.  The preconditioner only has to be a good
+// approximation of A^-1 (every solve still stops on the reference criterion in FP64), so its four
+// DST contractions run on FP16 operands with FP32 accumulation: legacy mma.sync m16n8k16 (SASS
+// HMMA.16816.F32) at ~555 TF/s on B200 against 37 TF/s for FP64 DMMA (tools/lowp_peak.cu).
+// Precision (tools/lowp_precond.py): the DST matrix needs ~10 significant bits (bf16's 8 cost up to
+// +7 % PCG iterations), the data tolerates bf16; FP16 (11 bits) for both reproduces the FP64
+// iteration counts.  FP16's range is handled by power-of-two scaling: the stage input r is scaled to
+// max|r| ~ 2^6 (the group maximum travels with the entry barrier) and the diagonal stage by a bound
+// of max 1/d(s); conversions saturate (satfinite) instead of overflowing, and ~20 octaves of headroom
+// remain above FP16's subnormal range.  The scales are exact powers of two and are undone in FP64.
+// During P^-1 the FP64 operand tile is dead, so its region holds the FP16 tile Vh [NP][SH] (row j =
+// true grid row, column i, zero outside the grid) and the DST matrix S [NP][SH] (row alpha-1, column
+// kappa-1, zero beyond n; square grids: one matrix serves both directions), copied in from L2 with one
+// TMA bulk copy per application.  Operand fragments come from ldmatrix (A: the matrix; B: Vh,
+// transposed for the y-stage).
+// ----------------------------------------------------------------------------
+template <class C>
+struct Lp {
+  static constexpr int SH = C::NP + 8;     // row stride (fp16): 16-byte rows, 8 rows hit 8 distinct bank quads
+  static constexpr int TILE = C::NP * SH;  // elements of Vh and of the matrix
+  static constexpr uint32_t TILE_BYTES = 2 * TILE;
+  static_assert(2 * TILE_BYTES <= sizeof(double) * C::VT, "fp16 tiles must fit in the operand tile region");
+  static_assert(TILE_BYTES % 16 == 0, "bulk copy granularity");
+};
+
+__device__ __forceinline__ void hmma_f16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr)
+               : "memory");
+}
+
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr)
+               : "memory");
+}
+
+// two floats -> packed fp16x2 (lo in the low half), saturating at +-65504
+__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+__device__ __forceinline__ uint16_t to_f16(float x) {
+  return static_cast<uint16_t>(pack_f16x2(x, 0.0f) & 0xffffu);
+}
+
+// x-direction, transposed mapping: out^T[i][j] = sum_k Sx[i][k] Vh[j][k] for i in unit column tm and
+// j over the rows of units tn .. tn + WC-1 (output layout as dst_xT).  K runs over all NP columns.
+template <class C>
+__device__ __forceinline__ void dst_xT_lp(uint32_t vh, uint32_t sx, float (&acc)[C::NF][4], int tm, int tn,
+                                          int lane) {
+  using L = Lp<C>;
+#pragma unroll
+  for (int nf = 0; nf < C::NF; ++nf)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[nf][e] = 0.f;
+  const int q = lane >> 3, r = lane & 7;
+  const uint32_t a_addr = sx + 2u * ((16 * tm + r + 8 * (q & 1)) * L::SH + 8 * (q >> 1));
+  uint32_t b_addr[C::NF / 2];
+#pragma unroll
+  for (int p = 0; p < C::NF / 2; ++p) {
+    const int nf = 2 * p + (q >> 1);
+    const int j = trow<C>(tn + (nf >> 1), 8 * (nf & 1) + r);
+    b_addr[p] = vh + 2u * (j * L::SH + 8 * (q & 1));
+  }
+#pragma unroll 2
+  for (int k0 = 0; k0 < C::NP; k0 += 16) {
+    uint32_t a[4];
+    ldsm_x4(a, a_addr + 2u * k0);
+#pragma unroll
+    for (int p = 0; p < C::NF / 2; ++p) {
+      uint32_t b[4];
+      ldsm_x4(b, b_addr[p] + 2u * k0);
+      hmma_f16(acc[2 * p], a, b[0], b[1]);
+      hmma_f16(acc[2 * p + 1], a, b[2], b[3]);
+    }
+  }
+}
+
+// y-direction, normal mapping: out[j][i] = sum_l Sy[j][l] Vh[l][i] for the rows of unit row urow and the
+// columns of units ucol .. ucol + WC-1 (output layout as dst_y).
+template <class C>
+__device__ __forceinline__ void dst_y_lp(uint32_t vh, uint32_t sy, float (&acc)[C::NF][4], int urow, int ucol,
+                                         int lane) {
+  using L = Lp<C>;
+#pragma unroll
+  for (int nf = 0; nf < C::NF; ++nf)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[nf][e] = 0.f;
+  const int q = lane >> 3, r = lane & 7;
+  const uint32_t a_addr = sy + 2u * (prow<C>(urow, r + 8 * (q & 1)) * L::SH + 8 * (q >> 1));
+  uint32_t b_addr[C::NF / 2];
+#pragma unroll
+  for (int p = 0; p < C::NF / 2; ++p)
+    b_addr[p] = vh + 2u * ((r + 8 * (q & 1)) * L::SH + 16 * ucol + 8 * (2 * p + (q >> 1)));
+#pragma unroll 2
+  for (int k0 = 0; k0 < C::NP; k0 += 16) {
+    uint32_t a[4];
+    ldsm_x4(a, a_addr + 2u * k0);
+#pragma unroll
+    for (int p = 0; p < C::NF / 2; ++p) {
+      uint32_t b[4];
+      ldsm_x4_t(b, b_addr[p] + 2u * k0 * L::SH);
+      hmma_f16(acc[2 * p], a, b[0], b[1]);
+      hmma_f16(acc[2 * p + 1], a, b[2], b[3]);
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
 // Cluster broadcast of each CTA's region of the operand tile (bulk async copies).
 // Every CTA owns a band of the output units; after it has written its band of
 // Vt it pushes the band into every peer's Vt with cp.async.bulk
@@ -411,6 +532,8 @@ struct Bcast {
   uint32_t mbar;   // shared::cta address of this CTA's mbarrier
   uint32_t phase;  // parity of the next phase to wait for
   uint32_t vt;     // shared::cta address of Vt
+  uint32_t mbar2;  // second mbarrier (this CTA only): bulk loads of the FP16 DST matrix
+  uint32_t phase2;
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -428,49 +551,65 @@ __device__ __forceinline__ void bcast_setup(Bcast<C>& b, double* Vt, uint64_t* m
   b.mbar = smem_addr(mbar);
   b.vt = smem_addr(Vt);
   b.phase = 0;
-  if constexpr (C::G > 1) {
-    if (tid == 0) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b.mbar));
-      asm volatile("fence.mbarrier_init.release.cluster;");
-    }
+  b.mbar2 = smem_addr(mbar + 1);
+  b.phase2 = 0;
+  if (tid == 0) {
+    if constexpr (C::G > 1) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b.mbar));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b.mbar2));
+    asm volatile("fence.mbarrier_init.release.cluster;");
   }
 }
 
-// Region of Vt owned by CTA `rank`: nseg segments of seg_bytes starting at seg_off(t).
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t& phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tLAB_WAIT2:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra LAB_WAIT2;\n\t}" ::"r"(mbar),
+      "r"(phase)
+      : "memory");
+  phase ^= 1;
+}
+
+// Region of a tile owned by CTA `rank`: nseg segments of seg_bytes starting at seg_off(t).
 // A contiguous band when the CTA owns an even number of unit rows (or no permutation is used);
 // otherwise 16 row segments (full rows, or half rows when two CTAs share a unit row).
-template <class C>
-struct BcastShape {
+// Tile geometry: ESZ-byte elements, row stride STRIDE, element (j, i) at (j + ROW0) * STRIDE + i + COL0.
+template <class C, int ESZ, int STRIDE, int ROW0, int COL0>
+struct BcastShapeT {
   static constexpr bool BAND = (C::G <= C::UR) && (!C::FOLD || (C::CR % 2 == 0));
   static constexpr int NSEG = BAND ? 1 : 16;
-  static constexpr uint32_t SEG_BYTES = BAND ? sizeof(double) * C::CR * 16 * C::S
-                                             : (C::G <= C::UR ? sizeof(double) * C::S : sizeof(double) * C::CC * 16);
+  static constexpr uint32_t SEG_BYTES = BAND ? ESZ * C::CR * 16 * STRIDE
+                                             : (C::G <= C::UR ? ESZ * STRIDE : ESZ * C::CC * 16);
+  static __device__ __forceinline__ uint32_t seg_off(int rank, int t) {
+    if constexpr (BAND) {
+      return static_cast<uint32_t>(ESZ * (rank * C::CR * 16 + ROW0) * STRIDE);
+    } else if constexpr (C::G <= C::UR) {
+      const int r = prow<C>(rank * C::CR, t);
+      return static_cast<uint32_t>(ESZ * (r + ROW0) * STRIDE);
+    } else {
+      constexpr int per = C::G / C::UR;
+      const int r = prow<C>(rank / per, t);
+      const int c0 = (rank % per) * C::CC * 16;
+      return static_cast<uint32_t>(ESZ * ((r + ROW0) * STRIDE + c0 + COL0));
+    }
+  }
 };
 
+// the FP64 operand tile Vt (halo row and columns, vt_idx)
 template <class C>
-__device__ __forceinline__ uint32_t bcast_seg_off(int rank, int t) {
-  using SH = BcastShape<C>;
-  if constexpr (SH::BAND) {
-    return static_cast<uint32_t>(sizeof(double) * (rank * C::CR * 16 + 1) * C::S);
-  } else if constexpr (C::G <= C::UR) {
-    const int r = prow<C>(rank * C::CR, t);
-    return static_cast<uint32_t>(sizeof(double) * (r + 1) * C::S);
-  } else {
-    constexpr int per = C::G / C::UR;
-    const int r = prow<C>(rank / per, t);
-    const int c0 = (rank % per) * C::CC * 16;
-    return static_cast<uint32_t>(sizeof(double) * ((r + 1) * C::S + c0 + 2));
-  }
-}
+using BcastShape = BcastShapeT<C, 8, C::S, 1, 2>;
 
-// Call after this CTA's threads wrote their elements of Vt (own band only): pushes the band to every
-// peer (bcast_wait then waits for the peers' bands).
+// the FP16 tile Vh of the low-precision preconditioner (Lp)
 template <class C>
-__device__ __forceinline__ void bcast_issue(Bcast<C>& b, int rank, int tid) {
+using BcastShapeLp = BcastShapeT<C, 2, Lp<C>::SH, 0, 0>;
+
+// Call after this CTA's threads wrote their elements of the tile at shared::cta address `base` (own band
+// only): pushes the band to every peer (bcast_wait then waits for the peers' bands).
+template <class C, class SH>
+__device__ __forceinline__ void bcast_issue_tile(Bcast<C>& b, uint32_t base, int rank, int tid) {
   if constexpr (C::G == 1) {
     __syncthreads();
   } else {
-    using SH = BcastShape<C>;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     if (tid == 0) {
@@ -478,18 +617,23 @@ __device__ __forceinline__ void bcast_issue(Bcast<C>& b, int rank, int tid) {
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b.mbar), "r"(incoming) : "memory");
     }
     if (tid < SH::NSEG) {
-      const uint32_t off = bcast_seg_off<C>(rank, tid);
+      const uint32_t off = SH::seg_off(rank, tid);
 #pragma unroll 1
       for (int q = 0; q < C::G; ++q) {
         if (q == rank) continue;
         asm volatile(
             "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                cluster_addr(b.vt + off, q)),
-            "r"(b.vt + off), "r"(SH::SEG_BYTES), "r"(cluster_addr(b.mbar, q))
+                cluster_addr(base + off, q)),
+            "r"(base + off), "r"(SH::SEG_BYTES), "r"(cluster_addr(b.mbar, q))
             : "memory");
       }
     }
   }
+}
+
+template <class C>
+__device__ __forceinline__ void bcast_issue(Bcast<C>& b, int rank, int tid) {
+  bcast_issue_tile<C, BcastShape<C>>(b, b.vt, rank, tid);
 }
 
 template <class C>

@@ -150,6 +150,8 @@ struct Smem {
   double* tabx;
   double* taby;
   double* red_peer[C::G];
+  double* mx;
+  double* mx_peer[C::G];
 };
 
 // z = P^{-1} r for the tau preconditioner: T1 = R Sx; T2 = Sy T1 * dinv; T3 = T2 Sx; z = Sy T3.
@@ -221,6 +223,140 @@ __device__ __forceinline__ void apply_tau(const Ctx<C>& c, const Smem<C>& sm, Bc
   }
 }
 
+// Same preconditioner with the DST contractions on FP16 tensor-core MMAs (rm_device.cuh, Lp): the FP64
+// tile region holds the FP16 tile and the DST matrix (bulk-copied from L2 per application).
+// z = Sy (Sx-stage (Sy (Sx-stage r s1)) * dinv s2) / (s1 s2), FP32 accumulation, returned as FP64 in acc;
+// s1 = 2^(6 - ilogb max|r|) (group maximum), s2 = 2^-ilogb(dbound), dbound >= max 1/d(s).
+// A group barrier on entry: peers push FP16 bands into this CTA's tile region, which aliases FP64 rows
+// that its threads may still read just before the call; the warp maxima of |r| travel with it.
+template <class C>
+__device__ __forceinline__ void apply_tau_lp(const Ctx<C>& c, const Smem<C>& sm, Bcast<C>& bc,
+                                             const double (&r)[C::WR][C::NF][4], double (&acc)[C::WR][C::NF][4],
+                                             const double* __restrict__ dinv, int nx, int ny,
+                                             const uint16_t* __restrict__ gs, double dbound, long long* timing) {
+  using L = Lp<C>;
+  static_assert(C::WR == 1, "DST stages assume one unit row per warp");
+  static_assert(C::G * C::WARPS <= 64, "max slots");
+  uint16_t* vh = reinterpret_cast<uint16_t*>(sm.Vt);
+  const uint32_t vh_s = smem_addr(vh);
+  const uint32_t s_s = vh_s + L::TILE_BYTES;  // square grids: one matrix serves both directions
+#ifdef RM_TIMING
+  struct {
+    long long* timing;
+  } P{timing};
+#endif
+  RM_T0();
+  double m = 0.0;
+#pragma unroll
+  for (int nf = 0; nf < C::NF; ++nf)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) m = fmax(m, fabs(r[0][nf][e]));
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if (c.lane == 0) {
+#pragma unroll
+    for (int q = 0; q < C::G; ++q) sm.mx_peer[q][c.rank * C::WARPS + c.warp] = m;
+  }
+  group_sync<C::G>();
+  if (c.tid == 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bc.mbar2), "r"(L::TILE_BYTES)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     s_s),
+                 "l"(gs), "r"(L::TILE_BYTES), "r"(bc.mbar2)
+                 : "memory");
+  }
+  double gm = 0.0;
+  for (int t = c.lane; t < C::G * C::WARPS; t += 32) gm = fmax(gm, sm.mx[t]);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) gm = fmax(gm, __shfl_xor_sync(0xffffffffu, gm, off));
+  const int e1 = gm > 0.0 ? 6 - ilogb(gm) : 0;
+  const int e2 = dbound > 0.0 ? -ilogb(dbound) : 0;
+  const double s1 = ldexp(1.0, e1), s2 = ldexp(1.0, e2), unscale = ldexp(1.0, -e1 - e2);
+  // r s1 -> Vh (own units; zero outside the grid)
+#pragma unroll
+  for (int nf = 0; nf < C::NF; ++nf)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = elem_row<C>(c, 0, 2 * h), i = elem_col<C>(c, nf, 2 * h);
+      const bool in = j < ny;
+      const float lo = (in && i < nx) ? (float)(r[0][nf][2 * h] * s1) : 0.f;
+      const float hi = (in && i + 1 < nx) ? (float)(r[0][nf][2 * h + 1] * s1) : 0.f;
+      *reinterpret_cast<uint32_t*>(vh + j * L::SH + i) = pack_f16x2(lo, hi);
+    }
+  RM_T(8);
+  mbar_wait(bc.mbar2, bc.phase2);
+  float a32[C::NF][4];
+#pragma unroll 1
+  for (int pass = 0; pass < 2; ++pass) {
+    if constexpr (C::G > C::UR) {
+      // two CTAs share each own row (column halves): exchange the halves
+      bcast_issue_tile<C, BcastShapeLp<C>>(bc, vh_s, c.rank, c.tid);
+      bcast_wait<C>(bc);
+    } else {
+      __syncthreads();
+    }
+    dst_xT_lp<C>(vh_s, s_s, a32, c.tm, c.tn, c.lane);
+    if constexpr (C::G > C::UR)
+      group_sync<C::G>();  // the row-sharing peer received our half and finished reading its copy
+    else
+      __syncthreads();
+    RM_T(9);
+#pragma unroll
+    for (int nf = 0; nf < C::NF; ++nf)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int j = elemT_row<C>(c, nf, e), i = 16 * c.tm + c.gq + 8 * (e >> 1);
+        vh[j * L::SH + i] = to_f16(a32[nf][e]);
+      }
+    bcast_issue_tile<C, BcastShapeLp<C>>(bc, vh_s, c.rank, c.tid);
+    bcast_wait<C>(bc);
+    RM_T(10);
+    dst_y_lp<C>(vh_s, s_s, a32, c.urow, c.ucol, c.lane);
+    RM_T(11);
+    if (pass == 1) break;
+    double dv[C::NF][4];
+#pragma unroll
+    for (int nf = 0; nf < C::NF; ++nf)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) dv[nf][e] = __ldcg(dinv + elem_sidx<C>(c, 0, nf, e)) * s2;
+    group_sync<C::G>();  // every CTA done reading its tile before peers push the next band
+#pragma unroll
+    for (int nf = 0; nf < C::NF; ++nf)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = elem_row<C>(c, 0, 2 * h), i = elem_col<C>(c, nf, 2 * h);
+        const bool in = j < ny;
+        const float lo = (in && i < nx) ? (float)(a32[nf][2 * h] * dv[nf][2 * h]) : 0.f;
+        const float hi = (in && i + 1 < nx) ? (float)(a32[nf][2 * h + 1] * dv[nf][2 * h + 1]) : 0.f;
+        *reinterpret_cast<uint32_t*>(vh + j * L::SH + i) = pack_f16x2(lo, hi);
+      }
+    RM_T(12);
+  }
+#pragma unroll
+  for (int nf = 0; nf < C::NF; ++nf)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[0][nf][e] = (double)a32[nf][e] * unscale;
+  // restore the zero halo / padding of the FP64 tile rows the FP16 data overwrote (the matvec reads
+  // them; the interior is rewritten with the next operand by the caller)
+  __syncthreads();
+  {
+    constexpr int touched = (2 * (int)L::TILE_BYTES + 8 * C::S - 1) / (8 * C::S);
+    double* Vt = sm.Vt;
+    for (int R = c.tid; R < touched; R += C::THREADS) {
+      double* row = Vt + R * C::S;
+      if (R == 0 || R > ny) {
+        for (int k = 0; k < C::S; ++k) row[k] = 0.0;
+      } else {
+        row[0] = 0.0;
+        row[1] = 0.0;
+        for (int k = nx + 2; k < C::S; ++k) row[k] = 0.0;
+      }
+    }
+  }
+}
+
 template <class C, bool PRE>
 __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P) {
   static_assert(C::SMEM <= 227 * 1024, "shared memory budget");
@@ -232,8 +368,9 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
   sm.xs = sm.red + C::RED;         // this CTA's part of the previous search direction (PCG)
   sm.tabx = sm.xs + C::XS;         // DST sine tables
   sm.taby = sm.tabx + C::ST;
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(sm.taby + C::ST);
-  int* sched = reinterpret_cast<int*>(mbar + 1);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(sm.taby + C::ST);  // [0] band exchange, [1] DST matrix
+  int* sched = reinterpret_cast<int*>(mbar + 2);
+  sm.mx = reinterpret_cast<double*>(mbar) + 8;  // [G * WARPS] warp maxima of |r| (low-precision tau)
   double* Vt = sm.Vt;
   double* gens = sm.gens;
   double* red = sm.red;
@@ -275,12 +412,14 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
   int* sched_peer[C::G];
   if constexpr (C::G == 1) {
     sm.red_peer[0] = red;
+    sm.mx_peer[0] = sm.mx;
     sched_peer[0] = sched;
   } else {
     auto cl = cgx::this_cluster();
 #pragma unroll
     for (int q = 0; q < C::G; ++q) {
       sm.red_peer[q] = cl.map_shared_rank(red, q);
+      sm.mx_peer[q] = cl.map_shared_rank(sm.mx, q);
       sched_peer[q] = cl.map_shared_rank(sched, q);
     }
   }
@@ -315,6 +454,15 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
 
   double acc[C::WR][C::NF][4];  // operator output of the current matvec / DST stage
   double rr_[C::WR][C::NF][4];  // CG residual r (register resident)
+  // z = P^-1 r into acc: FP16 tensor-core DST stages (precond 2) or FP64 DMMA (precond 1)
+  const bool lp_dst = W.precond == 2;
+  double lp_dbound = 1.0;  // >= max_i 1/d_i(s) of the current step
+  auto tau_apply = [&](const double(&rin)[C::WR][C::NF][4]) {
+    if (lp_dst)
+      apply_tau_lp<C>(c, sm, bc, rin, acc, dinv, nx, ny, P.dst16, lp_dbound, P.timing);
+    else
+      apply_tau<C>(c, sm, bc, rin, acc, dinv, nx, ny, Lx, Ly, P.timing);
+  };
 
   for (;;) {
     if (c.rank == 0 && c.tid == 0) {
@@ -332,6 +480,10 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
     bool in_tile = false;  // previous step left this step's input in Vt
     for (int n = n0; n <= n1; ++n) {
       const double s = 0.5 * W.d_dt[n - 1];
+      if (lp_dst) {
+        const double dlow = P.lp_dmin + s * P.lp_kmin;
+        lp_dbound = dlow > 0.0 ? 1.0 / dlow : 0.0;
+      }
       const double fs = W.d_f ? (W.d_fscale ? W.d_fscale[n] : 1.0) : 0.0;
       const double* Fn = W.d_f ? W.d_f + (int64_t)n * W.f_stride : nullptr;
 
@@ -401,7 +553,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
       buf ^= 1;
       const double bnorm = sqrt(tot[0]);
       const double target = bnorm > 0.0 ? W.rel_tol * bnorm : W.rel_tol;
-      if (W.d_guess && sqrt(tot[1]) > target) {
+      if (W.d_guess && W.x0_mode != 3 && sqrt(tot[1]) > target) {
         // second candidate start x0' = guess_n [- G_n] (the value this solve is about to replace);
         // keep whichever initial residual is smaller (deterministic: both norms are group-reduced)
         const double* Gr = W.d_gadd ? W.d_gadd + (int64_t)n * W.gadd_stride : nullptr;
@@ -436,11 +588,20 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
       int64_t its = 0;
       int fail = 0;
       bool done = res <= target;
+      if (W.x0_mode == 3) {
+        // preconditioner probe: y = P^-1 b, no CG (the host checks it against precond.py)
+        if constexpr (PRE) {
+          tau_apply(rr_);
+          ++npc;
+          RM_FOR_ELEM { xs[elem_xidx<C>(c, mr, nf, e)] = acc[mr][nf][e]; }
+        }
+        done = true;
+      }
 
       if (!done) {
         if constexpr (PRE) {
           // z = P^-1 r, p = z, rz = r.z
-          apply_tau<C>(c, sm, bc, rr_, acc, dinv, nx, ny, Lx, Ly, P.timing);
+          tau_apply(rr_);
           ++npc;
           double p1[1][C::WR][C::WC];
           zero_part<C>(p1[0]);
@@ -533,7 +694,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
         double red2[2];
         if constexpr (PRE) {
           // z = P^-1 r; reduce r.r (convergence test) and r.z together
-          apply_tau<C>(c, sm, bc, rr_, acc, dinv, nx, ny, Lx, Ly, P.timing);
+          tau_apply(rr_);
           ++npc;
           RM_TM();
           RM_FOR_ELEM { part2[1][mr][nf >> 1] += rr_[mr][nf][e] * acc[mr][nf][e]; }
@@ -594,7 +755,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
             break;
           }
           if constexpr (PRE) {
-            apply_tau<C>(c, sm, bc, rr_, acc, dinv, nx, ny, Lx, Ly, P.timing);
+            tau_apply(rr_);
             ++npc;
             zero_part<C>(p1[0]);
             RM_FOR_ELEM { p1[0][mr][nf >> 1] += rr_[mr][nf][e] * acc[mr][nf][e]; }

@@ -210,9 +210,10 @@ class Engine:
             raise TypeError("counters must be an int64 CUDA tensor of length 4")
         sw.d_counters = counters.data_ptr()
         sw.group = int(group)
-        if precond == "tau":
+        if precond in ("tau", "tau64"):
+            # 'tau': DST stages on FP16 tensor cores (FP32 accumulation); 'tau64': the same in FP64
             self.ensure_tau()
-            sw.precond = 1
+            sw.precond = 2 if precond == "tau" else 1
         elif precond != "none":
             raise ValueError(f"unknown preconditioner {precond!r}")
         if self.trace is not None:
@@ -228,6 +229,17 @@ class Engine:
         if self.trace is not None:
             e1.record()
             self.trace.append((tag, e0, e1, before, counters.clone(), nchains))
+
+    def precond_apply(self, V: torch.Tensor, dt: torch.Tensor, precond: str = "tau") -> torch.Tensor:
+        """z[b] = P(dt[b])^-1 V[b] for the tau preconditioner (probe of the solver's preconditioner; tests)."""
+        V = V.reshape(-1, self.ndof).contiguous()
+        B = V.shape[0]
+        out = torch.empty_like(V)
+        cnt = torch.zeros(4, dtype=torch.int64, device=V.device)
+        dt = dt.reshape(-1).to(torch.float64).contiguous()  # step n = 1..B uses dt[n-1]
+        self.sweep(nchains=B, first=1, cstride=1, clen=1, nmax=B, dt=dt, counters=cnt, rel_tol=1.0,
+                   explicit=False, x0_mode=3, f=(V, -1), f_stride=self.ndof, out=(out, -1), precond=precond)
+        return out
 
     def check_fail(self) -> None:
         """Raise CgFailure for the first failed solve since the last reset (synchronises)."""

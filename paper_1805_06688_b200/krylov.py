@@ -24,7 +24,9 @@ class CgOptions:
 
     Extension: ``preconditioner`` = 'tau' (default) runs CG preconditioned by
     the optimal sine-transform approximation of the step operator
-    (precond.py); 'none' is the reference's unpreconditioned CG.  Both stop on
+    (precond.py), its DST stages on FP16 tensor cores with FP32 accumulation;
+    'tau64' is the same preconditioner in FP64; 'none' is the reference's
+    unpreconditioned CG.  Both stop on
     the reference criterion ||b - A x|| <= rel_tol ||b|| with the same
     true-residual acceptance, so solutions agree to the solve tolerance; only
     the iteration counts differ.
@@ -38,8 +40,8 @@ class CgOptions:
     def __post_init__(self):
         if self.rel_tol <= 0:
             raise ValueError("relative tolerance must be positive")
-        if self.preconditioner not in ("tau", "none"):
-            raise ValueError("preconditioner must be 'tau' or 'none'")
+        if self.preconditioner not in ("tau", "tau64", "none"):
+            raise ValueError("preconditioner must be 'tau', 'tau64' or 'none'")
 
 
 class CgFailure(RuntimeError):

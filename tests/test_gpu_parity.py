@@ -81,7 +81,7 @@ def test_apply_accepts_device_batches(golden):
 
 
 # ----------------------------------------------------------------------------- CG
-PRECONDS = ["none", "tau"]
+PRECONDS = ["none", "tau", "tau64"]
 
 
 @pytest.mark.parametrize("pre", PRECONDS)
@@ -345,3 +345,31 @@ def test_tau_preconditioner_cuts_iterations(dt):
     assert per_point_rel(out["tau"][0], out["none"][0]).max() <= 1e-10
     assert out["tau"][1] * 2 <= out["none"][1] or dt < 1e-3
     assert out["tau"][1] < out["none"][1]
+    # FP16 DST stages (FP32 accumulation) leave the PCG iteration count essentially unchanged
+    assert abs(out["tau"][1] - out["tau64"][1]) <= max(1, 0.05 * out["tau64"][1])
+    assert per_point_rel(out["tau"][0], out["tau64"][0]).max() <= 1e-10
+
+
+@pytest.mark.parametrize("M,cfg", [(6, "cfg1"), (16, "cfg1"), (32, "cfg1"), (64, "cfg2"), (128, "cfg2")])
+def test_preconditioner_probe_matches_numpy(M, cfg):
+    """z = P(s)^-1 b from the device (rm_sweep x0_mode 3) against precond.py's tau diagonals and dense DST
+    matrices: FP64 DST stages to rounding, FP16 stages (FP32 accumulation) to FP16 accuracy."""
+    from paper_1805_06688_b200.engine import Engine
+    from paper_1805_06688_b200.precond import dst_matrix, tau_diagonals
+
+    case = make_case(cfg, M=M, Nt=8)
+    g = case.grid
+    eng = Engine.for_problem(g, case.beta, case.gamma, case.kx, case.ky)
+    dm, dk = tau_diagonals(g, case.beta, case.gamma, case.kx, case.ky)
+    Sx, Sy = dst_matrix(g.nx), dst_matrix(g.ny)
+    rng = np.random.default_rng(M)
+    V = rng.standard_normal((3, g.ndof)) * np.array([[1.0], [1e-9], [1e6]])
+    dts = np.array([1.0 / 4096, 1.0 / 64, 0.5])
+    ref = np.stack([(Sy @ ((Sy @ v.reshape(g.ny, g.nx) @ Sx) / (dm + 0.5 * dt * dk)) @ Sx).ravel()
+                    for v, dt in zip(V, dts)])
+    Vd, dtd = torch.from_numpy(V).cuda(), torch.from_numpy(dts).cuda()
+    z64 = eng.precond_apply(Vd, dtd, "tau64").cpu().numpy()
+    z16 = eng.precond_apply(Vd, dtd, "tau").cpu().numpy()
+    for k in range(3):
+        assert rel(z64[k], ref[k]) <= 1e-12, (k, rel(z64[k], ref[k]))
+        assert rel(z16[k], ref[k]) <= 5e-3, (k, rel(z16[k], ref[k]))
