@@ -35,7 +35,7 @@ import numpy as np  # noqa: E402
 
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
-from paper_1805_06688_b200.flops import fmv, fpc  # noqa: E402
+from paper_1805_06688_b200.flops import FP16_MMA_SYNC_PEAK_TFLOPS, fmv, fpc, fpc_dense  # noqa: E402
 
 PROFILES = os.path.join(REPO, "profiles")
 METRIC = "MGRIT fine-step space-time DOF/s (ndof*Nt / time-to-solution to 1e-8 residual)"
@@ -302,8 +302,19 @@ def run_ours(args):
     k_ms = sum(a.elapsed_time(b) for _, a, b, *_ in trace)
     mvs = sum(int((after - before)[2].item()) for _, _, _, before, after, _ in trace)
     pcs = sum(int((after - before)[3].item()) for _, _, _, before, after, _ in trace)
-    flops = mvs * fmv(case.grid.nx, case.grid.ny, eng.flags) + pcs * fpc(case.grid.nx, case.grid.ny)
-    achieved = flops / (k_ms * 1e-3) / 1e12
+    # the chain kernel mixes FP64 DMMA (operator applies) with FP16 HMMA (tau DST stages, 'tau'):
+    # its time bound is F64 / P64 + F16 / P16, so the roofline peak is the FLOP-weighted harmonic mean
+    # of the two measured peaks and frac = bound / measured time
+    f64 = mvs * fmv(case.grid.nx, case.grid.ny, eng.flags)
+    lp = args.precond == "tau" and case.grid.nx == case.grid.ny <= 127  # FP16 stages: square grids <= 127^2
+    if lp:
+        f16 = pcs * fpc_dense(case.grid.nx, case.grid.ny)
+    else:
+        f64 += pcs * fpc(case.grid.nx, case.grid.ny)
+        f16 = 0.0
+    t_bound = f64 / (peak * 1e12) + f16 / (FP16_MMA_SYNC_PEAK_TFLOPS * 1e12)
+    peak_mixed = (f64 + f16) / t_bound / 1e12
+    achieved = (f64 + f16) / (k_ms * 1e-3) / 1e12
     traffic, traffic_launch = ncu_traffic()
 
     # end to end through the public API (host inputs, host result)
@@ -347,13 +358,20 @@ def run_ours(args):
             "e2e": {"value": work / (e2e * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches // args.steps,
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "chain_kernel (FP64 DMMA block-Toeplitz matvec + fused CG)",
-                         "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (FP64 not in MEASURED_PEAKS.json)",
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_mixed, "unit": "TFLOP/s",
+                         "frac": achieved / peak_mixed, "traffic": traffic,
+                         "kernel": "chain_kernel (FP64 DMMA block-Toeplitz matvec + fused PCG, tau DST stages "
+                                   "on FP16 HMMA)",
+                         "peak_source": "FLOP-weighted harmonic mean of the FP64 peak (cuBLAS DGEMM 8192^3 "
+                                        "measured in this run; FP64 is not in MEASURED_PEAKS.json) and the legacy "
+                                        "mma.sync FP16 peak (tools/lowp_peak.cu, profiles/r01_lowp_peak.txt)",
+                         "fp64_peak": peak, "fp16_peak": FP16_MMA_SYNC_PEAK_TFLOPS,
+                         "fp64_flops_per_step": f64, "fp16_flops_per_step": f16,
+                         "fp64_achieved_over_kernel_time": f64 / (k_ms * 1e-3) / 1e12,
                          "traffic_launch": traffic_launch,
                          "flops_per_apply": fmv(case.grid.nx, case.grid.ny, eng.flags), "applies_per_step": mvs,
-                         "flops_per_precond": fpc(case.grid.nx, case.grid.ny),
+                         "flops_per_precond": fpc_dense(case.grid.nx, case.grid.ny) if lp
+                         else fpc(case.grid.nx, case.grid.ny),
                          "precond_applies_per_step": pcs,
                          "kernel_ms_per_step": k_ms},
             "clocks": clocks.summary(),

@@ -22,3 +22,13 @@ def fpc(nx: int, ny: int) -> float:
     """One tau-preconditioner application: two even/odd-folded DST-I contractions per direction
     (half the dense count), the folds and the diagonal scaling."""
     return 2.0 * nx * ny * (nx + ny) + 5.0 * nx * ny
+
+
+def fpc_dense(nx: int, ny: int) -> float:
+    """One tau-preconditioner application as the FP16 tensor-core path executes it: four unfolded
+    DST-I contractions (rm_device.cuh Lp), 2 n^3 each on an n x n grid, plus the diagonal scaling."""
+    return 4.0 * nx * ny * (nx + ny) + nx * ny
+
+
+# legacy mma.sync m16n8k16 FP16 -> FP32 on B200, measured with tools/lowp_peak.cu (profiles/r01_lowp_peak.txt)
+FP16_MMA_SYNC_PEAK_TFLOPS = 555.0
