@@ -35,7 +35,7 @@ import numpy as np  # noqa: E402
 
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
-from paper_1805_06688_b200.flops import FP16_MMA_SYNC_PEAK_TFLOPS, fmv, fpc, fpc_dense  # noqa: E402
+from paper_1805_06688_b200.flops import FP16_MMA_SYNC_PEAK_TFLOPS, fmv, fmv_split16, fpc, fpc_dense  # noqa: E402
 
 PROFILES = os.path.join(REPO, "profiles")
 METRIC = "MGRIT fine-step space-time DOF/s (ndof*Nt / time-to-solution to 1e-8 residual)"
@@ -302,13 +302,14 @@ def run_ours(args):
     k_ms = sum(a.elapsed_time(b) for _, a, b, *_ in trace)
     mvs = sum(int((after - before)[2].item()) for _, _, _, before, after, _ in trace)
     pcs = sum(int((after - before)[3].item()) for _, _, _, before, after, _ in trace)
+    mvs16 = sum(int((after - before)[4].item()) for _, _, _, before, after, _ in trace)
     # the chain kernel mixes FP64 DMMA (operator applies) with FP16 HMMA (tau DST stages, 'tau'):
     # its time bound is F64 / P64 + F16 / P16, so the roofline peak is the FLOP-weighted harmonic mean
     # of the two measured peaks and frac = bound / measured time
     f64 = mvs * fmv(case.grid.nx, case.grid.ny, eng.flags)
-    lp = args.precond == "tau" and case.grid.nx == case.grid.ny <= 127  # FP16 stages: square grids <= 127^2
+    lp = args.precond in ("tau", "tau16") and case.grid.nx == case.grid.ny <= 127  # FP16 stages: square <= 127^2
     if lp:
-        f16 = pcs * fpc_dense(case.grid.nx, case.grid.ny)
+        f16 = pcs * fpc_dense(case.grid.nx, case.grid.ny) + mvs16 * fmv_split16(case.grid.nx, case.grid.ny)
     else:
         f64 += pcs * fpc(case.grid.nx, case.grid.ny)
         f16 = 0.0
@@ -360,8 +361,9 @@ def run_ours(args):
             "gpu_launches": launches // args.steps,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_mixed, "unit": "TFLOP/s",
                          "frac": achieved / peak_mixed, "traffic": traffic,
-                         "kernel": "chain_kernel (FP64 DMMA block-Toeplitz matvec + fused PCG, tau DST stages "
-                                   "on FP16 HMMA)",
+                         "kernel": "chain_kernel (fused PCG: FP64 DMMA block-Toeplitz applies for right-hand "
+                                   "sides and true residuals, split-FP16 HMMA applies inside the iteration, tau "
+                                   "DST stages on FP16 HMMA)",
                          "peak_source": "FLOP-weighted harmonic mean of the FP64 peak (cuBLAS DGEMM 8192^3 "
                                         "measured in this run; FP64 is not in MEASURED_PEAKS.json) and the legacy "
                                         "mma.sync FP16 peak (tools/lowp_peak.cu, profiles/r01_lowp_peak.txt)",
@@ -373,6 +375,8 @@ def run_ours(args):
                          "flops_per_precond": fpc_dense(case.grid.nx, case.grid.ny) if lp
                          else fpc(case.grid.nx, case.grid.ny),
                          "precond_applies_per_step": pcs,
+                         "split_fp16_applies_per_step": mvs16,
+                         "flops_per_split_fp16_apply": fmv_split16(case.grid.nx, case.grid.ny),
                          "kernel_ms_per_step": k_ms},
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,
@@ -394,7 +398,7 @@ def main():
     ap.add_argument("--nt", type=int, default=None)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--precond", choices=["tau", "tau64", "none"], default="tau",
+    ap.add_argument("--precond", choices=["tau", "tau16", "tau64", "none"], default="tau",
                     help="inner CG: tau-preconditioned (default) or the reference's plain CG")
     args = ap.parse_args()
     if args.impl == "reference":

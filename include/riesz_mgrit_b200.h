@@ -106,15 +106,17 @@ RM_API int rm_apply_batched(const rm_grid* grid, int which, int batch, const dou
  * spacetime_residual (:187-205), each as one launch.
  * d_counters[0] += number of spatial solves, d_counters[1] += CG iterations
  * (Discretization.spatial_solves / cg_iterations, stepper.py:95-96,114,121),
- * d_counters[2] += operator applies performed, d_counters[3] += preconditioner applications
- * (FLOP accounting; the array must hold 4 counters).
+ * d_counters[2] += FP64 operator applies performed, d_counters[3] += preconditioner applications,
+ * d_counters[4] += split-FP16 operator applies (lp_matvec) (FLOP accounting; the array must hold 5
+ * counters).
  * A CG failure is recorded in the grid's failure slot (rm_fail_info).
  */
 typedef struct rm_sweep {
   int nchains, first, cstride, clen, nmax;
   int explicit_rhs; /* 0/1 */
   int x0_mode;      /* 0 zero, 1 warm (in_n), 2 d_x0; 3 = preconditioner probe: x = P^-1 b_n, no CG
-                       (needs precond > 0; grids up to 127^2) */
+                       (needs precond > 0; grids up to 127^2); 4 = split-FP16 apply probe: x = (M + s K) b
+                       through the in-iteration apply (needs precond 2 and lp_matvec; 63^2 .. 127^2) */
   int out_div;
   const double* d_dt;
   const double* d_src;
@@ -148,6 +150,10 @@ typedef struct rm_sweep {
      (the residual sweep keeps the C-relaxation values the next cycle would recompute).  NULL: off. */
   double* d_keep;
   int64_t keep_stride;
+  /* 1: inside the PCG iteration (precond 2), apply the operator to the search direction as a three-term
+     split-FP16 tensor-core product (~2^-22 relative; rm_device.cuh Mx), every stopping decision still on
+     the FP64 true residual; grids 63^2 .. 127^2 (others ignore the flag).  0: FP64 throughout. */
+  int lp_matvec;
 } rm_sweep;
 
 RM_API int rm_sweep_run(rm_grid* grid, const rm_sweep* sweep, void* stream);

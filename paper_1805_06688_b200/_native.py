@@ -44,6 +44,7 @@ class Sweep(C.Structure):
         ("d_guess", C.c_void_p),
         ("guess_stride", C.c_int64),
         ("d_keep", C.c_void_p), ("keep_stride", C.c_int64),
+        ("lp_matvec", C.c_int),
     ]
 
 

@@ -296,7 +296,7 @@ class CombinedStepOperator:
 
     def _device_solve(self, rhs, x0, opts: CgOptions):
         b, kind = to_device_2d(rhs, self.ndof)
-        counters = torch.zeros(4, dtype=torch.int64, device=b.device)
+        counters = torch.zeros(5, dtype=torch.int64, device=b.device)
         x = device_implicit_solve(self._engine, 2.0 * self.half_dt, b, x0, opts, counters)
         return from_device(x, kind), int(counters[1].item())
 

@@ -64,6 +64,7 @@ struct rm_grid {
   double* d_tab = nullptr;  // sine tables x then y
   uint16_t* d_dst16 = nullptr;  // FP16 DST-I matrix [np][np+8] (chain kernel, precond 2, nx == ny)
   double lp_dmin = 0.0, lp_kmin = 0.0;  // min over the grid of the tau diagonals dm, dk
+  double gen_absmax = 0.0;               // max |entry| of the six generator tables
   int max_clusters[5] = {0, 0, 0, 0, 0};
 };
 
@@ -163,6 +164,7 @@ int rm_grid_create(int nx, int ny, const double* t1x_col, const double* t1x_row,
     maxc = std::max(maxc, n);
   }
   g->scratch_clusters = maxc;
+  for (double v : tab) g->gen_absmax = std::max(g->gen_absmax, fabs(v));
   if ((e = cudaMalloc(&g->d_gens, sizeof(double) * tab.size())) != cudaSuccess ||
       (e = cudaMemcpy(g->d_gens, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice)) != cudaSuccess ||
       (e = cudaMalloc(&g->d_scratch, sizeof(double) * scratch_per_cluster * maxc)) != cudaSuccess ||
@@ -268,7 +270,9 @@ int rm_sweep_run(rm_grid* g, const rm_sweep* sw, void* stream) {
   if (sw->clen < 1 || sw->first < 1 || sw->nmax < sw->first) return fail(RM_EINVAL, "rm_sweep_run: bad chain shape");
   if (sw->out_div < 1) return fail(RM_EINVAL, "rm_sweep_run: out_div must be >= 1");
   if ((sw->explicit_rhs || sw->x0_mode == 1) && !sw->d_src) return fail(RM_EINVAL, "rm_sweep_run: d_src required");
-  if (sw->x0_mode < 0 || sw->x0_mode > 3) return fail(RM_EINVAL, "rm_sweep_run: x0_mode must be 0..3");
+  if (sw->x0_mode < 0 || sw->x0_mode > 4) return fail(RM_EINVAL, "rm_sweep_run: x0_mode must be 0..4");
+  if (sw->x0_mode == 4 && (sw->precond != 2 || !sw->lp_matvec || rm::big_supported(g->np) || g->nx != g->ny))
+    return fail(RM_EUNSUP, "rm_sweep_run: x0_mode 4 (split-FP16 apply probe) needs precond 2 with lp_matvec");
   if (sw->x0_mode == 3 && (!sw->precond || rm::big_supported(g->np)))
     return fail(RM_EUNSUP, "rm_sweep_run: x0_mode 3 (preconditioner probe) needs precond > 0 and a grid up to 127^2");
   if (sw->x0_mode == 2 && !sw->d_x0) return fail(RM_EINVAL, "rm_sweep_run: d_x0 required for x0_mode 2");
@@ -287,7 +291,8 @@ int rm_sweep_run(rm_grid* g, const rm_sweep* sw, void* stream) {
     a.sw = *sw;
     if (a.sw.precond == 2) a.sw.precond = 1;  // the large-grid kernel runs its DST stages in FP64 (for now)
     a.dst16 = nullptr;
-    a.lp_dmin = a.lp_kmin = 0.0;
+    a.lp_dmin = a.lp_kmin = a.gen_absmax = 0.0;
+    a.sw.lp_matvec = 0;
     a.nx = g->nx;
     a.ny = g->ny;
     a.cm = g->cm;
@@ -327,6 +332,7 @@ int rm_sweep_run(rm_grid* g, const rm_sweep* sw, void* stream) {
   a.dst16 = g->d_dst16;
   a.lp_dmin = g->lp_dmin;
   a.lp_kmin = g->lp_kmin;
+  a.gen_absmax = g->gen_absmax;
   if (a.sw.precond == 2 && !g->d_dst16) a.sw.precond = 1;  // nx != ny: DST stages in FP64
   a.nx = g->nx;
   a.ny = g->ny;

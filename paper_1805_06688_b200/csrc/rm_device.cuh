@@ -521,6 +521,189 @@ __device__ __forceinline__ void dst_y_lp(uint32_t vh, uint32_t sy, float (&acc)[
 }
 
 // ----------------------------------------------------------------------------
+// Split-FP16 operator apply for the PCG iterations (Mx).  The solve's stopping test is the reference's
+// FP64 criterion on the TRUE residual ||b - A x|| (computed with the FP64 DMMA apply, krylov.py:71-83),
+// so the search-direction products A p inside the iteration only need to be accurate to well below the
+// contraction the iteration achieves: they run as a three-term split product
+//     A p ~= T_hi P_hi + T_lo P_hi + T_hi P_lo       (T = hi + lo, P = hi + lo, FP16 each, FP32 accumulation)
+// on legacy mma.sync m16n8k16 (15x the FP64 DMMA rate per FLOP), ~2^-22 relative.  The fine-level step
+// operator is well conditioned (kappa ~ 5 at dt = 1/4096, ~400 at the coarsest dt of cfg2), so the
+// recursive residual tracks the true one to ~1e-6 relative and solves that need more than that are
+// finished by the reference's own restart from the true residual.
+// Operand layout (in the FP64 tile region, which is dead while the iteration runs on P):
+//   data tiles P_hi, P_lo [NP+2][SHD] fp16: row j+1 = grid row j (zero rows -1 and >= ny), column i+COL0
+//     (zero for i < 0 and i >= nx), scaled by 2^ep (max|p| <= bound ~ 2^14);
+//   pair tables PT[t][part][PL] (fp16x2): PT[d] = (t(d), t(d-1)) of the six per-step Toeplitz tables
+//     (rm_device.cuh build_step_tables: x diag / +1 / -1 rows, y diag / +1 / -1 columns), scaled by 2^et.
+// x-direction (M = j, N = i, K = k): A = P rows j + {0, +1, -1} (ldmatrix), B = PT of gx0, gxp, gxm.
+// y-direction (M = j, N = i, K = l): A = PT of gy0 / gyp / gym at d = j - l, B = P rows l (ldmatrix.trans);
+//   the column shifts of the off-diagonal blocks (P[l][i +- 1]) are applied to the OUTPUT: W = T P over
+//   aligned columns with one extra fragment, then Y[j][i] += W[j][i +- 1] by warp shuffles.
+// ----------------------------------------------------------------------------
+template <class C>
+struct Mx {
+  static constexpr int COL0 = 8;                     // left pad (W_- reads one fragment left of column 0)
+  static constexpr int SHD = C::NP + 24;             // columns [-8, NP+16); 16-byte rows, conflict-free ldmatrix
+  static constexpr int ROWS = C::NP + 2;             // rows -1 .. NP
+  static constexpr int TILE = ROWS * SHD;            // fp16 elements per tile
+  static constexpr uint32_t TILE_BYTES = 2 * TILE;
+  static constexpr int PD0 = C::NP + 12;             // pair-table index of d = 0
+  static constexpr int PL = 2 * C::NP + 24;          // d in [-(NP+12), NP+12)
+  static constexpr uint32_t PT_OFF = 2 * TILE_BYTES;  // byte offset of the pair tables in the FP64 tile region
+  static constexpr uint32_t PT_BYTES = 6 * 2 * PL * 4;
+  static constexpr bool ENABLED = C::NP >= 64 && PT_OFF + PT_BYTES <= sizeof(double) * C::VT &&
+                                  PT_OFF >= 2 * Lp<C>::TILE_BYTES;  // tau's FP16 tiles stay below the tables
+  static_assert((SHD * 2) % 16 == 0, "ldmatrix rows must be 16-byte aligned");
+};
+
+__device__ __forceinline__ void ldsm_x2_t(uint32_t (&r)[2], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];\n"
+               : "=r"(r[0]), "=r"(r[1])
+               : "r"(addr)
+               : "memory");
+}
+
+// x -> (hi, lo) fp16 with hi + lo ~ x to ~22 bits (x already scaled into FP16 range)
+__device__ __forceinline__ void split_f16(double x, float& hi, float& lo) {
+  const float xf = (float)x;
+  const uint32_t h = pack_f16x2(xf, 0.0f);
+  hi = __half2float(__ushort_as_half(static_cast<unsigned short>(h & 0xffffu)));
+  lo = xf - hi;
+}
+
+// Pair tables of the current step's implicit-side Toeplitz tables (gens, FP64 [6][GL]), scaled by 2^et.
+template <class C>
+__device__ __forceinline__ void build_pair_tables(uint32_t* __restrict__ pt, const double* __restrict__ gens,
+                                                  double st, int tid) {
+  using X = Mx<C>;
+  for (int idx = tid; idx < 6 * X::PL; idx += C::THREADS) {
+    const int t = idx / X::PL, d = idx - t * X::PL - X::PD0;
+    auto tv = [&](int dd) -> double {
+      const int g = dd + C::NP;  // gens entry (dd + NP), dd in [-NP, NP+8)
+      return (g >= 0 && g < C::GL) ? gens[t * C::GL + g] * st : 0.0;
+    };
+    float h0, l0, h1, l1;
+    split_f16(tv(d), h0, l0);
+    split_f16(tv(d - 1), h1, l1);
+    pt[(2 * t) * X::PL + d + X::PD0] = pack_f16x2(h0, h1);
+    pt[(2 * t + 1) * X::PL + d + X::PD0] = pack_f16x2(l0, l1);
+  }
+}
+
+// One y-direction segment: out[f] (+)= sum_l t_SG(j - l) P[l][16 ucol + 8 f + n] over NFR column fragments
+// starting at byte offset brow (per lane: ldmatrix.trans row address of row l0 + r (+8)).
+template <class C, int SG, int NFR>
+__device__ __forceinline__ void matvec_lp_y(uint32_t hi_t, uint32_t lo_t, const uint32_t* __restrict__ pt,
+                                            uint32_t brow, int ja, int jb, int tig, float (&out)[NFR][4]) {
+  using X = Mx<C>;
+  if constexpr (SG > 0) {
+#pragma unroll
+    for (int f = 0; f < NFR; ++f)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) out[f][e] = 0.f;
+  }
+  const uint32_t* th = pt + (2 * (3 + SG)) * X::PL + X::PD0 - 2 * tig;
+  const uint32_t* tl = th + X::PL;
+#pragma unroll 2
+  for (int l0 = 0; l0 < C::NP; l0 += 16) {
+    uint32_t ah[4], al[4];
+    ah[0] = th[ja - l0];
+    ah[1] = th[jb - l0];
+    ah[2] = th[ja - l0 - 8];
+    ah[3] = th[jb - l0 - 8];
+    al[0] = tl[ja - l0];
+    al[1] = tl[jb - l0];
+    al[2] = tl[ja - l0 - 8];
+    al[3] = tl[jb - l0 - 8];
+    const uint32_t b0 = brow + 2u * l0 * X::SHD;
+#pragma unroll
+    for (int f = 0; f < NFR; ++f) {
+      uint32_t bh[2], bl[2];
+      ldsm_x2_t(bh, hi_t + b0 + 16u * f);
+      ldsm_x2_t(bl, lo_t + b0 + 16u * f);
+      hmma_f16(out[f], al, bh[0], bh[1]);
+      hmma_f16(out[f], ah, bl[0], bl[1]);
+      hmma_f16(out[f], ah, bh[0], bh[1]);
+    }
+  }
+}
+
+// acc[nf][e] (normal mapping, FP32, scaled by 2^(ep+et)) = (A p) over this warp's units.
+// vt: shared address of the FP64 tile region (data tiles at 0 / TILE_BYTES); pt: pair tables.
+template <class C>
+__device__ __forceinline__ void matvec_lp(uint32_t vt, const uint32_t* __restrict__ pt, float (&acc)[C::NF][4],
+                                          int urow, int ucol, int gq, int tig, int lane) {
+  using X = Mx<C>;
+  constexpr int NF = C::NF;
+#pragma unroll
+  for (int nf = 0; nf < NF; ++nf)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[nf][e] = 0.f;
+  const int q = lane >> 3, r = lane & 7;
+  const uint32_t hi_t = vt, lo_t = vt + X::TILE_BYTES;
+  // ---- x-direction: three row segments (0, +1 with gxp, -1 with gxm)
+  {
+    const int jr = prow<C>(urow, r + 8 * (q & 1));  // this lane's ldmatrix row (grid row of the unit)
+    const int dbase = 16 * ucol + gq - 2 * tig + X::PD0;
+#pragma unroll 1
+    for (int sg = 0; sg < 3; ++sg) {
+      const int dj = sg == 0 ? 0 : (sg == 1 ? 1 : -1);
+      const uint32_t arow = 2u * ((jr + dj + 1) * X::SHD + X::COL0 + 8 * (q >> 1));
+      const uint32_t* th = pt + (2 * sg) * X::PL + dbase;
+      const uint32_t* tl = th + X::PL;
+#pragma unroll 2
+      for (int k0 = 0; k0 < C::NP; k0 += 16) {
+        uint32_t ah[4], al[4];
+        ldsm_x4(ah, hi_t + arow + 2u * k0);
+        ldsm_x4(al, lo_t + arow + 2u * k0);
+        // B of n-fragment nf: b0 = PT[d], b1 = PT[d-8], d = 16 ucol + 8 nf + gq - k0 - 2 tig
+        uint32_t bh[NF + 1], bl[NF + 1];
+#pragma unroll
+        for (int f = 0; f <= NF; ++f) {
+          bh[f] = th[8 * f - 8 - k0];
+          bl[f] = tl[8 * f - 8 - k0];
+        }
+#pragma unroll
+        for (int nf = 0; nf < NF; ++nf) {
+          hmma_f16(acc[nf], al, bh[nf + 1], bh[nf]);
+          hmma_f16(acc[nf], ah, bl[nf + 1], bl[nf]);
+          hmma_f16(acc[nf], ah, bh[nf + 1], bh[nf]);
+        }
+      }
+    }
+  }
+  // ---- y-direction
+  const int ja = prow<C>(urow, gq), jb = prow<C>(urow, gq + 8);
+  const uint32_t brow = 2u * ((r + 8 * (q & 1) + 1) * X::SHD + X::COL0 + 16 * ucol);
+  matvec_lp_y<C, 0, NF>(hi_t, lo_t, pt, brow, ja, jb, tig, acc);
+  float w[NF + 1][4];
+  // Y[j][i] += W[j][i+1], W over column fragments 0..NF
+  matvec_lp_y<C, 1, NF + 1>(hi_t, lo_t, pt, brow, ja, jb, tig, w);
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    acc[f][0] += w[f][1];
+    acc[f][2] += w[f][3];
+    const int src = tig < 3 ? lane + 1 : lane - 3;
+    const float v1 = __shfl_sync(0xffffffffu, tig == 0 ? w[f + 1][0] : w[f][0], src);
+    const float v3 = __shfl_sync(0xffffffffu, tig == 0 ? w[f + 1][2] : w[f][2], src);
+    acc[f][1] += v1;
+    acc[f][3] += v3;
+  }
+  // Y[j][i] += W[j][i-1], W over column fragments -1..NF-1 (w[g] = fragment g-1)
+  matvec_lp_y<C, 2, NF + 1>(hi_t, lo_t, pt, brow - 16u, ja, jb, tig, w);
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    acc[f][1] += w[f + 1][0];
+    acc[f][3] += w[f + 1][2];
+    const int src = tig > 0 ? lane - 1 : lane + 3;
+    const float v0 = __shfl_sync(0xffffffffu, tig == 3 ? w[f][1] : w[f + 1][1], src);
+    const float v2 = __shfl_sync(0xffffffffu, tig == 3 ? w[f][3] : w[f + 1][3], src);
+    acc[f][0] += v0;
+    acc[f][2] += v2;
+  }
+}
+
+// ----------------------------------------------------------------------------
 // Cluster broadcast of each CTA's region of the operand tile (bulk async copies).
 // Every CTA owns a band of the output units; after it has written its band of
 // Vt it pushes the band into every peer's Vt with cp.async.bulk
@@ -653,6 +836,52 @@ template <class C>
 __device__ __forceinline__ void bcast_band(Bcast<C>& b, int rank, int tid) {
   bcast_issue<C>(b, rank, tid);
   bcast_wait<C>(b);
+}
+
+// group_reduce plus a group-wide maximum of one nonnegative value per thread (channel 3 of the
+// reduction slots; the sums use channels 0..NV-1, NV <= 3).  Same single group barrier.
+template <class C, int NV>
+__device__ __forceinline__ void group_reduce_mx(double (&part)[NV][C::WR][C::WC], double mloc, double* red_local,
+                                                double* const* red_peer, int buf, int urow, int ucol, int lane,
+                                                double (&out)[NV], double& outmax) {
+  static_assert(NV <= 3, "channel 3 carries the maximum");
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+#pragma unroll
+    for (int mr = 0; mr < C::WR; ++mr)
+#pragma unroll
+      for (int uc = 0; uc < C::WC; ++uc) part[v][mr][uc] = warp_allsum(part[v][mr][uc]);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) mloc = fmax(mloc, __shfl_xor_sync(0xffffffffu, mloc, off));
+  if (lane == 0) {
+#pragma unroll
+    for (int mr = 0; mr < C::WR; ++mr)
+#pragma unroll
+      for (int uc = 0; uc < C::WC; ++uc) {
+        const int u = (urow + mr) * C::UR + ucol + uc;
+#pragma unroll
+        for (int q = 0; q < C::G; ++q) {
+#pragma unroll
+          for (int v = 0; v < NV; ++v) red_peer[q][buf * 4 * C::U + v * C::U + u] = part[v][mr][uc];
+          red_peer[q][buf * 4 * C::U + 3 * C::U + u] = mloc;
+        }
+      }
+  }
+  group_sync<C::G>();
+  const double* r = red_local + buf * 4 * C::U;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    double x = 0.0;
+    if (lane < C::U) x = r[v * C::U + lane];
+    if (lane + 32 < C::U) x += r[v * C::U + lane + 32];
+    out[v] = warp_allsum(x);
+  }
+  double m = 0.0;
+  if (lane < C::U) m = r[3 * C::U + lane];
+  if (lane + 32 < C::U) m = fmax(m, r[3 * C::U + lane + 32]);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+  outmax = m;
 }
 
 // Deterministic group-wide sum of NV values.  part[v][mr][uc] is this

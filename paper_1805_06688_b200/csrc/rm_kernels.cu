@@ -233,7 +233,8 @@ template <class C>
 __device__ __forceinline__ void apply_tau_lp(const Ctx<C>& c, const Smem<C>& sm, Bcast<C>& bc,
                                              const double (&r)[C::WR][C::NF][4], double (&acc)[C::WR][C::NF][4],
                                              const double* __restrict__ dinv, int nx, int ny,
-                                             const uint16_t* __restrict__ gs, double dbound, long long* timing) {
+                                             const uint16_t* __restrict__ gs, double dbound, bool restore,
+                                             long long* timing) {
   using L = Lp<C>;
   static_assert(C::WR == 1, "DST stages assume one unit row per warp");
   static_assert(C::G * C::WARPS <= 64, "max slots");
@@ -339,7 +340,9 @@ __device__ __forceinline__ void apply_tau_lp(const Ctx<C>& c, const Smem<C>& sm,
 #pragma unroll
     for (int e = 0; e < 4; ++e) acc[0][nf][e] = (double)a32[nf][e] * unscale;
   // restore the zero halo / padding of the FP64 tile rows the FP16 data overwrote (the matvec reads
-  // them; the interior is rewritten with the next operand by the caller)
+  // them; the interior is rewritten with the next operand by the caller).  Not needed when the next
+  // apply is the split-FP16 one (its caller restores the FP64 halo before any FP64 apply).
+  if (!restore) return;
   __syncthreads();
   {
     constexpr int touched = (2 * (int)L::TILE_BYTES + 8 * C::S - 1) / (8 * C::S);
@@ -356,6 +359,60 @@ __device__ __forceinline__ void apply_tau_lp(const Ctx<C>& c, const Smem<C>& sm,
     }
   }
 }
+
+// Zero every non-interior entry of the FP64 operand tile (halo rows / columns and the padding beyond
+// nx, ny): the FP64 apply and the mass stencil read them.  Needed after the split-FP16 iteration or the
+// FP16 preconditioner reused the tile region.  Touches no interior entry (peers' bands may be arriving).
+template <class C>
+__device__ __forceinline__ void vt_zero_halo(double* Vt, int nx, int ny, int tid) {
+  for (int R = tid; R < C::NP + 2; R += C::THREADS) {
+    double* row = Vt + R * C::S;
+    if (R == 0 || R > ny) {
+      for (int k = 0; k < C::S; ++k) row[k] = 0.0;
+    } else {
+      row[0] = 0.0;
+      row[1] = 0.0;
+      for (int k = nx + 2; k < C::S; ++k) row[k] = 0.0;
+    }
+  }
+}
+
+// Zero the halo rows and pad columns of both split-FP16 data tiles (this CTA's copy, all rows).
+template <class C>
+__device__ __forceinline__ void mx_zero_pads(double* Vt, int tid) {
+  using X = Mx<C>;
+  constexpr int RB = X::SHD * 2 / 16;  // 16-byte chunks per row
+  uint4* base = reinterpret_cast<uint4*>(Vt);
+  const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+  constexpr int FULL = 2 * 2 * RB;                    // rows -1 and NP of both tiles
+  constexpr int PADS = 2 * C::NP * 3;                 // 3 pad chunks per interior row (cols [-8,0), [NP,NP+16))
+  for (int idx = tid; idx < FULL + PADS; idx += C::THREADS) {
+    if (idx < FULL) {
+      const int t = idx / (2 * RB), rr = (idx / RB) % 2, ch = idx % RB;
+      base[t * (X::TILE_BYTES / 16) + (rr ? C::NP + 1 : 0) * RB + ch] = z;
+    } else {
+      const int k = idx - FULL, t = k / (3 * C::NP), rr = (k / 3) % C::NP + 1, ch = k % 3;
+      base[t * (X::TILE_BYTES / 16) + rr * RB + (ch == 0 ? 0 : RB - 3 + ch)] = z;
+    }
+  }
+}
+
+// the split-FP16 data tiles: each CTA's own rows of both tiles (hi, lo) in one exchange
+template <class C>
+struct BcastShapeMx {
+  using B = BcastShapeT<C, 2, Mx<C>::SHD, 1, Mx<C>::COL0>;
+  static constexpr int NSEG = 2 * B::NSEG;
+  static constexpr uint32_t SEG_BYTES = B::SEG_BYTES;
+  static __device__ __forceinline__ uint32_t seg_off(int rank, int t) {
+    return B::seg_off(rank, t >> 1) + (t & 1) * Mx<C>::TILE_BYTES;
+  }
+};
+
+// split-FP16 iteration: residual replacement once the recursive residual fell below this fraction of
+// the true residual at the last replacement (the apply is accurate to ~1e-5 for smooth directions)
+constexpr double kLpReplace = 1e-5;
+// split-FP16 iteration only for steps with s max|K| <= kLpMaxRatio * 6 cm (condition number ~< 10)
+constexpr double kLpMaxRatio = 4.0;
 
 template <class C, bool PRE>
 __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P) {
@@ -456,12 +513,58 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
   double rr_[C::WR][C::NF][4];  // CG residual r (register resident)
   // z = P^-1 r into acc: FP16 tensor-core DST stages (precond 2) or FP64 DMMA (precond 1)
   const bool lp_dst = W.precond == 2;
+  // split-FP16 search-direction applies inside the PCG iteration (Mx; with the FP16 preconditioner)
+  const bool lp_mv = Mx<C>::ENABLED && PRE && lp_dst && W.lp_matvec;
+  bool lp_step = false;  // this step runs the split-FP16 iteration (well-conditioned step operators only)
   double lp_dbound = 1.0;  // >= max_i 1/d_i(s) of the current step
   auto tau_apply = [&](const double(&rin)[C::WR][C::NF][4]) {
     if (lp_dst)
-      apply_tau_lp<C>(c, sm, bc, rin, acc, dinv, nx, ny, P.dst16, lp_dbound, P.timing);
+      apply_tau_lp<C>(c, sm, bc, rin, acc, dinv, nx, ny, P.dst16, lp_dbound, !lp_step, P.timing);
     else
       apply_tau<C>(c, sm, bc, rin, acc, dinv, nx, ny, Lx, Ly, P.timing);
+  };
+  // split-FP16 iteration state: power-of-two scales of the data (2^lp_ep, from a bound on max|p|) and of
+  // the pair tables (2^lp_et, per step); the tables are rebuilt whenever FP64 data overwrote them
+  uint32_t* lp_pt = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(Vt) + Mx<C>::PT_OFF);
+  int lp_ep = 0, lp_et = 0;
+  double lp_bp = 0.0;
+  double lp_rrep = 0.0;  // true residual norm at the solve start / last replacement
+  bool lp_true_next = false;  // the next iteration computes the true residual (FP64 apply)
+  bool lp_pt_ok = false;
+  // p = z [+ beta p_old] (z in acc): FP64 copy in pold_, split-FP16 copy in the data tiles (own units),
+  // pads zeroed, pair tables rebuilt if needed, own bands pushed to the peers (waited for in the apply)
+  auto lp_set_p = [&](double beta, bool with_old) {
+#pragma unroll
+    for (int nf = 0; nf < C::NF; ++nf)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = elem_row<C>(c, 0, 2 * h), i = elem_col<C>(c, nf, 2 * h);
+        double pv[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int e = 2 * h + u;
+          pv[u] = 0.0;
+          if (j < ny && i + u < nx) {
+            const int xi = elem_xidx<C>(c, 0, nf, e);
+            pv[u] = with_old ? acc[0][nf][e] + beta * pold_[xi] : acc[0][nf][e];
+            pold_[xi] = pv[u];
+          }
+        }
+        const double sc = ldexp(1.0, lp_ep);
+        float h0, l0, h1, l1;
+        split_f16(pv[0] * sc, h0, l0);
+        split_f16(pv[1] * sc, h1, l1);
+        uint32_t* hi = reinterpret_cast<uint32_t*>(reinterpret_cast<uint16_t*>(Vt) + (j + 1) * Mx<C>::SHD +
+                                                   Mx<C>::COL0 + i);
+        hi[0] = pack_f16x2(h0, h1);
+        hi[Mx<C>::TILE / 2] = pack_f16x2(l0, l1);
+      }
+    mx_zero_pads<C>(Vt, c.tid);
+    if (!lp_pt_ok) {
+      build_pair_tables<C>(lp_pt, gens, ldexp(1.0, lp_et), c.tid);
+      lp_pt_ok = true;
+    }
+    bcast_issue_tile<C, BcastShapeMx<C>>(bc, smem_addr(Vt), c.rank, c.tid);
   };
 
   for (;;) {
@@ -486,6 +589,14 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
       }
       const double fs = W.d_f ? (W.d_fscale ? W.d_fscale[n] : 1.0) : 0.0;
       const double* Fn = W.d_f ? W.d_f + (int64_t)n * W.f_stride : nullptr;
+      if (lp_mv) {
+        vt_zero_halo<C>(Vt, nx, ny, c.tid);  // the previous solve's FP16 data overwrote the FP64 tile
+        lp_et = 13 - ilogb(fabs(s) * P.gen_absmax + 6.0 * cm);  // max |table entry| < 2^14 after scaling
+        lp_pt_ok = false;
+        // the apply error grows with the step operator's condition number (~ s max|K| / (6 cm)):
+        // only well-conditioned steps (the fine levels) iterate in split FP16
+        lp_step = fabs(s) * P.gen_absmax <= kLpMaxRatio * 6.0 * cm;
+      }
 
       // ---------------- right-hand side, initial iterate and residual --------------
       // (the previous step ended with a group barrier: nobody reads the tables any more)
@@ -496,6 +607,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
         matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true, P.merge);
       }
       int64_t nmv = need_in ? 1 : 0;
+      int64_t nmv16 = 0;  // split-FP16 applies (lp_step)
       int64_t npc = 0;  // preconditioner applications
       double part[2][C::WR][C::WC];
       zero_part<C>(part[0]);
@@ -585,6 +697,8 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
       }
       double res = sqrt(tot[1]);
       double rr = tot[1];  // r.r (CG) or r.z (PCG)
+      lp_rrep = res;
+      lp_true_next = false;
       int64_t its = 0;
       int fail = 0;
       bool done = res <= target;
@@ -594,6 +708,28 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           tau_apply(rr_);
           ++npc;
           RM_FOR_ELEM { xs[elem_xidx<C>(c, mr, nf, e)] = acc[mr][nf][e]; }
+        }
+        done = true;
+      }
+      if (W.x0_mode == 4) {
+        // split-FP16 apply probe: y = (M + s K) b through the in-iteration path (b in the role of p)
+        if (lp_mv) {
+          RM_FOR_ELEM { acc[mr][nf][e] = rr_[mr][nf][e]; }
+          double mb = 0.0, one[1];
+          RM_FOR_ELEM { mb = fmax(mb, fabs(acc[mr][nf][e])); }
+          double p0[1][C::WR][C::WC];
+          zero_part<C>(p0[0]);
+          group_reduce_mx<C, 1>(p0, mb, red, sm.red_peer, buf, c.urow, c.ucol, c.lane, one, lp_bp);
+          buf ^= 1;
+          lp_ep = lp_bp > 0.0 ? 13 - ilogb(lp_bp) : 0;
+          lp_set_p(0.0, false);
+          bcast_wait<C>(bc);
+          float a32[C::NF][4];
+          matvec_lp<C>(smem_addr(Vt), lp_pt, a32, c.urow, c.ucol, c.gq, c.tig, c.lane);
+          const double inv = ldexp(1.0, -(lp_ep + lp_et));
+          RM_FOR_ELEM { xs[elem_xidx<C>(c, mr, nf, e)] = (double)a32[nf][e] * inv; }
+          ++nmv16;
+          group_sync<C::G>();
         }
         done = true;
       }
@@ -607,12 +743,25 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           zero_part<C>(p1[0]);
           RM_FOR_ELEM { p1[0][mr][nf >> 1] += rr_[mr][nf][e] * acc[mr][nf][e]; }
           double rz[1];
-          group_reduce<C, 1>(p1, red, sm.red_peer, buf, c.urow, c.ucol, c.lane, rz);
-          buf ^= 1;
-          rr = rz[0];
-          RM_FOR_ELEM {
-            const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
-            if (j < ny && i < nx) Vt[vt_idx<C>(j, i)] = acc[mr][nf][e];
+          if (lp_step) {
+            double mz = 0.0;
+            RM_FOR_ELEM { mz = fmax(mz, fabs(acc[mr][nf][e])); }
+            double gz;
+            group_reduce_mx<C, 1>(p1, mz, red, sm.red_peer, buf, c.urow, c.ucol, c.lane, rz, gz);
+            buf ^= 1;
+            rr = rz[0];
+            lp_bp = gz;
+            lp_ep = gz > 0.0 ? 13 - ilogb(gz) : 0;
+            lp_set_p(0.0, false);  // waited for inside the first apply
+          } else {
+            group_reduce<C, 1>(p1, red, sm.red_peer, buf, c.urow, c.ucol, c.lane, rz);
+            buf ^= 1;
+            rr = rz[0];
+            RM_FOR_ELEM {
+              const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
+              if (j < ny && i < nx) Vt[vt_idx<C>(j, i)] = acc[mr][nf][e];
+            }
+            bcast_issue<C>(bc, c.rank, c.tid);  // waited for inside the first matvec
           }
         } else {
           // p = r into the operand tile of every CTA of the group
@@ -620,8 +769,8 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
             const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
             if (j < ny && i < nx) Vt[vt_idx<C>(j, i)] = rr_[mr][nf][e];
           }
+          bcast_issue<C>(bc, c.rank, c.tid);  // waited for inside the first matvec
         }
-        bcast_issue<C>(bc, c.rank, c.tid);  // waited for inside the first matvec
       }
       if (c.tid == 0 && n < n1) {
         // the chain's next-step inputs: L2 resident by the time this solve finishes (each CTA of the
@@ -646,11 +795,20 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
         }
         RM_T(7);
         // Ap and p'Ap; the peers' bands of p arrive during the diagonal x segment (own rows only)
-        if constexpr (C::G > C::UR) bcast_wait<C>(bc);  // own rows are shared: nothing to overlap
-        matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true, P.merge, [&] {
-          if constexpr (C::G <= C::UR) bcast_wait<C>(bc);
-        });
-        ++nmv;
+        if (lp_step) {
+          bcast_wait<C>(bc);
+          float a32[C::NF][4];
+          matvec_lp<C>(smem_addr(Vt), lp_pt, a32, c.urow, c.ucol, c.gq, c.tig, c.lane);
+          const double inv = ldexp(1.0, -(lp_ep + lp_et));
+          RM_FOR_ELEM { acc[mr][nf][e] = (double)a32[nf][e] * inv; }
+          ++nmv16;
+        } else {
+          if constexpr (C::G > C::UR) bcast_wait<C>(bc);  // own rows are shared: nothing to overlap
+          matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true, P.merge, [&] {
+            if constexpr (C::G <= C::UR) bcast_wait<C>(bc);
+          });
+          ++nmv;
+        }
         RM_T(0);
         double p1[1][C::WR][C::WC];
         zero_part<C>(p1[0]);
@@ -659,7 +817,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           double ap = 0.0;
           if (j < ny && i < nx) {
             ap = acc[mr][nf][e];
-            p1[0][mr][nf >> 1] += Vt[vt_idx<C>(j, i)] * ap;
+            p1[0][mr][nf >> 1] += (lp_step ? pold_[elem_xidx<C>(c, mr, nf, e)] : Vt[vt_idx<C>(j, i)]) * ap;
           }
           acc[mr][nf][e] = ap;
         }
@@ -677,28 +835,58 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
         double part2[2][C::WR][C::WC];
         zero_part<C>(part2[0]);
         zero_part<C>(part2[1]);
+        const bool true_now = lp_step && lp_true_next;
         RM_FOR_ELEM {
           const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
           if (j < ny && i < nx) {
             const int xi = elem_xidx<C>(c, mr, nf, e);
-            const double pv = Vt[vt_idx<C>(j, i)];
+            const double pv = lp_step ? pold_[xi] : Vt[vt_idx<C>(j, i)];
             atomicAdd(xs + xi, alpha * pv);  // RED: no return value, no latency on the critical path
             const double rn = rr_[mr][nf][e] - alpha * acc[mr][nf][e];
             rr_[mr][nf][e] = rn;
-            part2[0][mr][nf >> 1] += rn * rn;
+            if (!true_now) part2[0][mr][nf >> 1] += rn * rn;
             // the preconditioner overwrites the operand tile: keep p for the direction update
-            if constexpr (PRE) pold_[xi] = pv;
+            if constexpr (PRE)
+              if (!lp_step) pold_[xi] = pv;
+          }
+        }
+        if (true_now) {
+          // split-FP16 iteration, predicted to cross the target or the replacement threshold: this
+          // iteration's residual is the TRUE one, b - A x with the FP64 apply (residual replacement; the
+          // search direction recurrence continues), so no preconditioner application is wasted
+          vt_zero_halo<C>(Vt, nx, ny, c.tid);
+          lp_pt_ok = false;
+          RM_FOR_ELEM {
+            const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
+            if (j < ny && i < nx) Vt[vt_idx<C>(j, i)] = xs[elem_xidx<C>(c, mr, nf, e)];
+          }
+          bcast_band<C>(bc, c.rank, c.tid);
+          matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true, P.merge);
+          ++nmv;
+          RM_FOR_ELEM {
+            const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
+            double rt = 0.0;
+            if (j < ny && i < nx) rt = sb_[elem_sidx<C>(c, mr, nf, e)] - acc[mr][nf][e];
+            rr_[mr][nf][e] = rt;
+            part2[0][mr][nf >> 1] += rt * rt;
           }
         }
         RM_T(3);
         double red2[2];
+        double lp_mz = 0.0;
         if constexpr (PRE) {
           // z = P^-1 r; reduce r.r (convergence test) and r.z together
           tau_apply(rr_);
           ++npc;
           RM_TM();
           RM_FOR_ELEM { part2[1][mr][nf >> 1] += rr_[mr][nf][e] * acc[mr][nf][e]; }
-          group_reduce<C, 2>(part2, red, sm.red_peer, buf, c.urow, c.ucol, c.lane, red2);
+          if (lp_step) {
+            double mz = 0.0;
+            RM_FOR_ELEM { mz = fmax(mz, fabs(acc[mr][nf][e])); }
+            group_reduce_mx<C, 2>(part2, mz, red, sm.red_peer, buf, c.urow, c.ucol, c.lane, red2, lp_mz);
+          } else {
+            group_reduce<C, 2>(part2, red, sm.red_peer, buf, c.urow, c.ucol, c.lane, red2);
+          }
         } else {
           double p0[1][C::WR][C::WC];
 #pragma unroll
@@ -713,14 +901,36 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
         buf ^= 1;
         RM_T(4);
         double rr_new = red2[0];
+        const double res_prev = res;
         res = sqrt(rr_new);
         if (!isfinite(res)) {
           fail = RM_CG_NONFINITE;
           its = k;
           break;
         }
-        if (res <= target) {
-          // acceptance on the true residual (krylov.py:71-83)
+        if (true_now) {
+          if (res <= target) {  // the reference criterion on the true residual
+            its = k;
+            done = true;
+            break;
+          }
+          lp_rrep = res;
+      lp_true_next = false;
+        }
+        if (lp_step) {
+          // next residual ~ res * (res / res_prev): make it the true one if it is predicted to cross the
+          // target or the replacement threshold
+          const double pred = res * fmin(1.0, res / res_prev);
+          lp_true_next = pred <= target || pred <= kLpReplace * lp_rrep;
+        }
+        if (res <= target && !true_now) {
+          // acceptance on the true residual (krylov.py:71-83), FP64 apply.  Split-FP16 iteration: also a
+          // residual replacement every kLpReplace of contraction (the recursive residual drifts from the
+          // true one by ~1e-5 of the residual at the last replacement), the search direction kept.
+          if (lp_step) {
+            vt_zero_halo<C>(Vt, nx, ny, c.tid);
+            lp_pt_ok = false;
+          }
           RM_FOR_ELEM {
             const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
             if (j < ny && i < nx) Vt[vt_idx<C>(j, i)] = xs[elem_xidx<C>(c, mr, nf, e)];
@@ -741,7 +951,8 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           group_reduce<C, 1>(p1, red, sm.red_peer, buf, c.urow, c.ucol, c.lane, tt);
           buf ^= 1;
           const double true_res = sqrt(tt[0]);
-          if (true_res <= fmax(target, 10.0 * res)) {
+          // the reference's acceptance; the split-FP16 iteration accepts only a true residual <= target
+          if (true_res <= (lp_step ? target : fmax(target, 10.0 * res))) {
             its = k;
             done = true;
             break;
@@ -760,6 +971,21 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
             zero_part<C>(p1[0]);
             RM_FOR_ELEM { p1[0][mr][nf >> 1] += rr_[mr][nf][e] * acc[mr][nf][e]; }
             double rz[1];
+            if (lp_step) {
+              // residual replacement: continue the direction recurrence from the true residual
+              double mz = 0.0;
+              RM_FOR_ELEM { mz = fmax(mz, fabs(acc[mr][nf][e])); }
+              double gz;
+              group_reduce_mx<C, 1>(p1, mz, red, sm.red_peer, buf, c.urow, c.ucol, c.lane, rz, gz);
+              buf ^= 1;
+              const double beta = rz[0] / rr;
+              rr = rz[0];
+              lp_rrep = true_res;
+              lp_bp = gz + fabs(beta) * lp_bp;
+              lp_ep = lp_bp > 0.0 ? 13 - ilogb(lp_bp) : 0;
+              lp_set_p(beta, true);
+              continue;
+            }
             group_reduce<C, 1>(p1, red, sm.red_peer, buf, c.urow, c.ucol, c.lane, rz);
             buf ^= 1;
             rr = rz[0];
@@ -776,6 +1002,15 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
         const double rho_new = red2[1];
         const double beta = rho_new / rr;
         rr = rho_new;
+        if (lp_step) {
+          // max|p| <= max|z| + beta max|p_old| (all CTAs hold the same bound)
+          lp_bp = lp_mz + fabs(beta) * lp_bp;
+          lp_ep = lp_bp > 0.0 ? 13 - ilogb(lp_bp) : 0;
+          lp_set_p(beta, true);
+          RM_T(5);
+          RM_T(6);
+          continue;
+        }
         RM_FOR_ELEM {
           const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
           if (j < ny && i < nx) {
@@ -796,6 +1031,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
         atomicAdd(W.d_counters + 1, (unsigned long long)its);
         atomicAdd(W.d_counters + 2, (unsigned long long)nmv);
         atomicAdd(W.d_counters + 3, (unsigned long long)npc);
+        if (lp_step) atomicAdd(W.d_counters + 4, (unsigned long long)nmv16);
       }
       if (fail) {
         if (c.rank == 0 && c.tid == 0 && atomicCAS(P.fail, 0, fail) == 0) {

@@ -28,6 +28,7 @@ struct ChainArgs {
   double* gbuf;        // ... and per-group reduction / broadcast slots (1024 doubles each)
   const uint16_t* dst16; // FP16 DST-I matrix [NP][NP+8] of the low-precision tau stages (precond 2, nx == ny)
   double lp_dmin, lp_kmin; // min over the grid of dm, dk: 1/(lp_dmin + s lp_kmin) bounds max 1/d(s)
+  double gen_absmax;       // max |entry| of the six generator tables (split-FP16 table scaling)
 };
 
 struct ApplyArgs {

@@ -206,14 +206,17 @@ class Engine:
         sw.d_keep, sw.keep_stride = _ptr(keep, row), row
         sw.rel_tol = float(rel_tol)
         sw.max_iter = -1 if max_iter is None else int(max_iter)
-        if counters.dtype != torch.int64 or not counters.is_cuda or counters.numel() < 4:
-            raise TypeError("counters must be an int64 CUDA tensor of length 4")
+        if counters.dtype != torch.int64 or not counters.is_cuda or counters.numel() < 5:
+            raise TypeError("counters must be an int64 CUDA tensor of length 5")
         sw.d_counters = counters.data_ptr()
         sw.group = int(group)
-        if precond in ("tau", "tau64"):
-            # 'tau': DST stages on FP16 tensor cores (FP32 accumulation); 'tau64': the same in FP64
+        if precond in ("tau", "tau16", "tau64"):
+            # 'tau64': tau-PCG in FP64; 'tau16': its DST stages on FP16 tensor cores (FP32 accumulation);
+            # 'tau': additionally the in-iteration applies A p as split-FP16 tensor-core products
+            # (every stopping decision stays on the FP64 true residual)
             self.ensure_tau()
-            sw.precond = 2 if precond == "tau" else 1
+            sw.precond = 1 if precond == "tau64" else 2
+            sw.lp_matvec = 1 if precond == "tau" else 0
         elif precond != "none":
             raise ValueError(f"unknown preconditioner {precond!r}")
         if self.trace is not None:
@@ -235,10 +238,21 @@ class Engine:
         V = V.reshape(-1, self.ndof).contiguous()
         B = V.shape[0]
         out = torch.empty_like(V)
-        cnt = torch.zeros(4, dtype=torch.int64, device=V.device)
+        cnt = torch.zeros(5, dtype=torch.int64, device=V.device)
         dt = dt.reshape(-1).to(torch.float64).contiguous()  # step n = 1..B uses dt[n-1]
         self.sweep(nchains=B, first=1, cstride=1, clen=1, nmax=B, dt=dt, counters=cnt, rel_tol=1.0,
                    explicit=False, x0_mode=3, f=(V, -1), f_stride=self.ndof, out=(out, -1), precond=precond)
+        return out
+
+    def lp_apply_probe(self, V: torch.Tensor, dt: torch.Tensor) -> torch.Tensor:
+        """(M + dt[b]/2 K) V[b] through the split-FP16 in-iteration apply (probe; tests)."""
+        V = V.reshape(-1, self.ndof).contiguous()
+        B = V.shape[0]
+        out = torch.empty_like(V)
+        cnt = torch.zeros(5, dtype=torch.int64, device=V.device)
+        dt = dt.reshape(-1).to(torch.float64).contiguous()
+        self.sweep(nchains=B, first=1, cstride=1, clen=1, nmax=B, dt=dt, counters=cnt, rel_tol=1.0,
+                   explicit=False, x0_mode=4, f=(V, -1), f_stride=self.ndof, out=(out, -1), precond="tau")
         return out
 
     def check_fail(self) -> None:

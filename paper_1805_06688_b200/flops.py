@@ -30,5 +30,11 @@ def fpc_dense(nx: int, ny: int) -> float:
     return 4.0 * nx * ny * (nx + ny) + nx * ny
 
 
+def fmv_split16(nx: int, ny: int) -> float:
+    """One split-FP16 operator apply inside the PCG iteration (rm_device.cuh Mx) as executed: three
+    unmerged Toeplitz segments per direction, each a three-term split product (hi*hi + lo*hi + hi*lo)."""
+    return 3.0 * (3 * 2.0 * nx * nx * ny + 3 * 2.0 * ny * ny * nx)
+
+
 # legacy mma.sync m16n8k16 FP16 -> FP32 on B200, measured with tools/lowp_peak.cu (profiles/r01_lowp_peak.txt)
 FP16_MMA_SYNC_PEAK_TFLOPS = 555.0

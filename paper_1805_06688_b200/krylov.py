@@ -24,12 +24,14 @@ class CgOptions:
 
     Extension: ``preconditioner`` = 'tau' (default) runs CG preconditioned by
     the optimal sine-transform approximation of the step operator
-    (precond.py), its DST stages on FP16 tensor cores with FP32 accumulation;
-    'tau64' is the same preconditioner in FP64; 'none' is the reference's
-    unpreconditioned CG.  Both stop on
-    the reference criterion ||b - A x|| <= rel_tol ||b|| with the same
-    true-residual acceptance, so solutions agree to the solve tolerance; only
-    the iteration counts differ.
+    (precond.py), its DST stages on FP16 tensor cores with FP32 accumulation
+    and the in-iteration operator applies A p as split-FP16 tensor-core
+    products (~2^-22 relative); 'tau16' keeps those applies in FP64; 'tau64'
+    is the same preconditioner entirely in FP64; 'none' is the reference's
+    unpreconditioned CG.  All stop on the reference criterion
+    ||b - A x|| <= rel_tol ||b|| with the same FP64 true-residual acceptance,
+    so solutions agree to the solve tolerance; only the iteration counts
+    differ.
     """
 
     rel_tol: float = 1e-9
@@ -40,8 +42,8 @@ class CgOptions:
     def __post_init__(self):
         if self.rel_tol <= 0:
             raise ValueError("relative tolerance must be positive")
-        if self.preconditioner not in ("tau", "tau64", "none"):
-            raise ValueError("preconditioner must be 'tau', 'tau64' or 'none'")
+        if self.preconditioner not in ("tau", "tau16", "tau64", "none"):
+            raise ValueError("preconditioner must be 'tau', 'tau16', 'tau64' or 'none'")
 
 
 class CgFailure(RuntimeError):

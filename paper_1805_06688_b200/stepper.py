@@ -95,7 +95,7 @@ class Discretization:
         self.time_quad_points = time_quad_points
         self.device = require_cuda()
         self.engine = engine or Engine.shared(grid, spec.beta, spec.gamma, spec.kx, spec.ky)
-        self.counters = torch.zeros(4, dtype=torch.int64, device=self.device)
+        self.counters = torch.zeros(5, dtype=torch.int64, device=self.device)
         self._combined: dict = {}
         self._mg = None
 

@@ -52,9 +52,9 @@ class CpuEngine:
                 except O.OracleCgFailure as exc:
                     if self.fail is None:
                         self.fail = (n, exc)
-                    counters += torch.tensor([1, exc.iterations, 0, 0])
+                    counters += torch.tensor([1, exc.iterations, 0, 0, 0])
                     break
-                counters += torch.tensor([1, its, its + 2, 0])
+                counters += torch.tensor([1, its, its + 2, 0, 0])
                 y = x
                 if gadd is not None:
                     y = _row(gadd, n).numpy() + y
@@ -95,7 +95,7 @@ class CpuDisc:
         self.cg_opts = cg_opts
         self.engine = engine or CpuEngine(spec.grid, spec.beta, spec.gamma, spec.kx, spec.ky)
         self.device = torch.device("cpu")
-        self.counters = torch.zeros(4, dtype=torch.int64)
+        self.counters = torch.zeros(5, dtype=torch.int64)
         self.ndof = spec.grid.ndof
 
     def device_loads(self, points):

@@ -32,7 +32,7 @@ for nch in a.chains:
     G_ = torch.zeros_like(U)
     dt = torch.full((N,), dtv, dtype=torch.float64, device="cuda")
     for rep in range(2):
-        cnt = torch.zeros(4, dtype=torch.int64, device="cuda")
+        cnt = torch.zeros(5, dtype=torch.int64, device="cuda")
         V = U.clone()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()

@@ -18,7 +18,7 @@ for nch, dtv in ((512, 1 / 4096), (64, 1 / 512), (8, 1 / 64), (1, 1 / 8)):
         res = []
         for Gs in (1, 2, 4, 8, 16):
             try:
-                cnt = torch.zeros(4, dtype=torch.int64, device="cuda")
+                cnt = torch.zeros(5, dtype=torch.int64, device="cuda")
                 V = U.clone()
                 eng.sweep(nchains=nch, first=1, cstride=8, clen=7, nmax=N, dt=dt, counters=cnt, rel_tol=1e-12,
                           src=V, x0_mode=1, gadd=G_, out=V, group=Gs, precond=pre)

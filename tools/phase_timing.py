@@ -25,7 +25,7 @@ def main():
         V = torch.from_numpy(np.random.default_rng(0).random((B, n))).cuda()
         dt = torch.full((B,), 1.0 / 4096, dtype=torch.float64, device="cuda")
         out = torch.empty_like(V)
-        cnt = torch.zeros(4, dtype=torch.int64, device="cuda")
+        cnt = torch.zeros(5, dtype=torch.int64, device="cuda")
         zero = (ctypes.c_longlong * 16)()
         eng.sweep(nchains=B, first=1, cstride=1, clen=1, nmax=B, dt=dt, counters=cnt, rel_tol=1e-12, src=V,
                   x0_mode=1, out=(out, -1), group=G, precond=PRE)

@@ -55,23 +55,26 @@ def main():
         for tag, e0, e1, before, after, nch in trace:
             ms = e0.elapsed_time(e1)
             d = (after - before).cpu().tolist()
-            s = agg.setdefault(tag, dict(launches=0, ms=0.0, solves=0, cg=0, mv=0, pc=0, chains=nch))
+            s = agg.setdefault(tag, dict(launches=0, ms=0.0, solves=0, cg=0, mv=0, mv16=0, pc=0, chains=nch))
             s["launches"] += 1
             s["ms"] += ms
             s["solves"] += d[0]
             s["cg"] += d[1]
             s["mv"] += d[2]
+            s["mv16"] += d[4]
             s["pc"] += d[3]
             tot_ms += ms
             tot_mv += d[2]
-            tot_fl += d[2] * F + d[3] * FP
+            tot_fl += (d[2] + d[4]) * F + d[3] * FP
         print(f"rep {rep}: {case.name} ndof={case.grid.ndof} Nt={case.tmesh.n_intervals} iters={tr.iterations} "
-              f"TTS={tts:.3f}s kernel_ms={tot_ms:.1f} matvecs={tot_mv} achieved={tot_fl / tot_ms / 1e9:.2f} TF/s")
+              f"TTS={tts:.3f}s kernel_ms={tot_ms:.1f} fp64_applies={tot_mv} "
+              f"algorithmic={tot_fl / tot_ms / 1e9:.2f} TF/s (FP64-equivalent)")
         for tag, s in agg.items():
             print(f"  {tag:12s} launches={s['launches']:4d} chains={s['chains']:5d} ms={s['ms']:9.2f} "
                   f"solves={s['solves']:7d} cg/solve={s['cg'] / max(s['solves'], 1):7.1f} "
                   f"pc/solve={s['pc'] / max(s['solves'], 1):5.1f} "
-                  f"TF/s={(s['mv'] * F + s['pc'] * FP) / max(s['ms'], 1e-9) / 1e9:6.2f}")
+                  f"fp64mv/solve={s['mv'] / max(s['solves'], 1):5.1f} "
+                  f"TF/s={((s['mv'] + s['mv16']) * F + s['pc'] * FP) / max(s['ms'], 1e-9) / 1e9:6.2f}")
         print("  residuals:", ["%.3e" % r for r in tr.residual_norms])
     if a.counts_json:
         lv = {}
