@@ -13,6 +13,7 @@ import os
 import re
 import subprocess
 import sys
+import tempfile
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(PKG)
@@ -73,12 +74,13 @@ def build(force: bool = False, verbose: bool = False, timing: bool = False) -> s
     os.makedirs(LIBDIR, exist_ok=True)
     extra = ["-DRM_TIMING"] if timing else []
     extra += [f"-D{d}" for d in os.environ.get("RM_DEFINES", "").split(",") if d]
+    objdir = tempfile.mkdtemp(prefix="rm_build_", dir=LIBDIR)  # private: concurrent builds do not collide
     jobs = []  # (label, source, defines, object)
     for src in SOURCES:
-        jobs.append((src, src, [], os.path.join(LIBDIR, src.replace(".cu", ".o"))))
+        jobs.append((src, src, [], os.path.join(objdir, src.replace(".cu", ".o"))))
     for np_, g in chain_cases():  # one translation unit per chain-kernel configuration
         jobs.append((f"rm_kernels.cu[{np_},{g}]", "rm_kernels.cu", [f"-DRM_CASE_NP={np_}", f"-DRM_CASE_G={g}"],
-                     os.path.join(LIBDIR, f"rm_chain_{np_}_{g}.o")))
+                     os.path.join(objdir, f"rm_chain_{np_}_{g}.o")))
     nproc = max(1, min(len(jobs), os.cpu_count() or 1))
     running, objs = [], []
     pending = list(jobs)
@@ -106,6 +108,7 @@ def build(force: bool = False, verbose: bool = False, timing: bool = False) -> s
     os.replace(tmp, out)
     for o in objs:
         os.remove(o)
+    os.rmdir(objdir)
     return out
 
 

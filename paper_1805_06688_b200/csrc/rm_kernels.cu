@@ -411,8 +411,8 @@ struct BcastShapeMx {
 // split-FP16 iteration: residual replacement once the recursive residual fell below this fraction of
 // the true residual at the last replacement (the apply is accurate to ~1e-5 for smooth directions)
 constexpr double kLpReplace = 1e-5;
-// split-FP16 iteration only for steps with s max|K| <= kLpMaxRatio * 6 cm (condition number ~< 10)
-constexpr double kLpMaxRatio = 4.0;
+// split-FP16 iteration only for steps with s max|K| <= kLpMaxRatio * 6 cm (condition number ~< 20)
+constexpr double kLpMaxRatio = 16.0;
 
 template <class C, bool PRE>
 __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P) {
