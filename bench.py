@@ -307,7 +307,7 @@ def run_ours(args):
     # its time bound is F64 / P64 + F16 / P16, so the roofline peak is the FLOP-weighted harmonic mean
     # of the two measured peaks and frac = bound / measured time
     f64 = mvs * fmv(case.grid.nx, case.grid.ny, eng.flags)
-    lp = args.precond in ("tau", "tau16") and case.grid.nx == case.grid.ny <= 127  # FP16 stages: square <= 127^2
+    lp = args.precond in ("tau", "tau16") and case.grid.nx == case.grid.ny  # FP16 DST stages: square grids
     if lp:
         f16 = pcs * fpc_dense(case.grid.nx, case.grid.ny) + mvs16 * fmv_split16(case.grid.nx, case.grid.ny)
     else:

@@ -139,7 +139,7 @@ typedef struct rm_sweep {
   int group;   /* CTAs per chain (cluster size); 0 = library choice */
   int precond; /* 0: plain CG (the reference algorithm); 1: tau-preconditioned CG (needs
                   rm_grid_set_tau), DST stages in FP64; 2: the same preconditioner with its DST stages
-                  on FP16 tensor cores (scaled, FP32 accumulation; square grids up to 127^2, others run 1);
+                  on FP16 tensor cores (scaled, FP32 accumulation; square grids, others run 1);
                   all stop on ||b - A x|| <= rel_tol ||b|| in FP64 */
   /* optional second starting guess x0' = guess_n - G_n (G_n only when d_gadd): the solve starts
      from whichever of x0, x0' has the smaller initial residual (e.g. the iterate value this step

@@ -451,6 +451,136 @@ __device__ __forceinline__ void big_reduce(double (&part)[NV][4], double* wred, 
   }
 }
 
+// ---- FP16 DST stages of the tau preconditioner (precond 2; see rm_device.cuh Lp) ----------------------
+// The stage inputs live in two FP16 copies V16a, V16b [NP][SHH] inside the (FP64) preconditioner temporary
+// pv1; the DST matrix S16 [NP][SHH] (row alpha-1, column kappa-1, zero beyond n) comes from the grid.
+// Each stage is a 128 x 128 x NP tile GEMM per CTA: K chunks of 64 (A: 128 rows of S16, B: 128 x 64 or
+// 64 x 128 of the vector) are staged by cp.async (double buffered) and fed to mma.sync m16n8k16 through
+// ldmatrix (transposed for the y-stage), FP32 accumulation.  Power-of-two scaling as in the small kernel.
+template <class C>
+struct BigLp {
+  static constexpr int SHH = C::NP + 8;  // global row stride (fp16), 16-byte rows
+  static constexpr int KC = 64;          // K chunk
+  static constexpr int AS = KC + 8;      // smem row stride of the A chunk / x-stage B chunk (== 4 words mod 32)
+  static constexpr int BYS = 128 + 8;    // smem row stride of the y-stage B chunk
+  static constexpr int ABYTES = 128 * AS * 2;
+  static constexpr int BBYTES = (128 * AS > KC * BYS ? 128 * AS : KC * BYS) * 2;
+  static constexpr int BUF = ABYTES + BBYTES;  // one pipeline buffer
+  static_assert(2 * BUF <= 2 * (int)sizeof(double) * C::STAGE, "FP16 stage buffers must fit the FP64 stage space");
+  static_assert(2 * (size_t)C::NP * SHH * 2 <= sizeof(double) * C::PV, "two FP16 vectors fit in pv1");
+};
+
+// A chunk: rows row0 .. row0+127 of S16, columns k0 .. k0+63 (8 x 16 B per row)
+template <class C>
+__device__ __forceinline__ void load_a16(char* st, const uint16_t* __restrict__ s16, int row0, int k0, int tid) {
+  using B = BigLp<C>;
+  for (int t = tid; t < 128 * 8; t += C::THREADS) {
+    const int r = t >> 3, q = t & 7;
+    cp_async16(st + (r * B::AS + 8 * q) * 2, s16 + (size_t)(row0 + r) * B::SHH + k0 + 8 * q);
+  }
+}
+// x-stage B chunk: rows R0 .. R0+127 of the vector, columns k0 .. k0+63
+template <class C>
+__device__ __forceinline__ void load_bx16(char* st, const uint16_t* __restrict__ v, int R0, int k0, int tid) {
+  using B = BigLp<C>;
+  for (int t = tid; t < 128 * 8; t += C::THREADS) {
+    const int r = t >> 3, q = t & 7;
+    cp_async16(st + (r * B::AS + 8 * q) * 2, v + (size_t)(R0 + r) * B::SHH + k0 + 8 * q);
+  }
+}
+// y-stage B chunk: rows k0 .. k0+63 of the vector, columns C0 .. C0+127 (16 x 16 B per row)
+template <class C>
+__device__ __forceinline__ void load_by16(char* st, const uint16_t* __restrict__ v, int k0, int C0, int tid) {
+  using B = BigLp<C>;
+  for (int t = tid; t < B::KC * 16; t += C::THREADS) {
+    const int r = t >> 4, q = t & 15;
+    cp_async16(st + (r * B::BYS + 8 * q) * 2, v + (size_t)(k0 + r) * B::SHH + C0 + 8 * q);
+  }
+}
+
+// One FP16 DST stage of the tile.  YST: out[j][i] = sum_l S[j][l] V[l][i] in the normal mapping (rows
+// R0 + big_urow(wr, .), columns C0 + 16 wc0 + .); else the transposed x-stage out^T[i][j] = sum_k S[i][k]
+// V[j][k] (i = C0 + 16 wr + ., j = R0 + 16 wc0 + .).
+template <class C, bool YST>
+__device__ __forceinline__ void big_dst16(const uint16_t* __restrict__ s16, const uint16_t* __restrict__ v,
+                                          char* stage, float (&acc)[8][4], const BigCtx& c) {
+  using B = BigLp<C>;
+#pragma unroll
+  for (int nf = 0; nf < 8; ++nf)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[nf][e] = 0.f;
+  const int row0 = YST ? c.R0 : c.C0;
+  const int q = c.lane >> 3, r = c.lane & 7;
+  const int arow = YST ? big_urow(c.wr, r + 8 * (q & 1)) : 16 * c.wr + r + 8 * (q & 1);
+  constexpr int NK = C::NP / B::KC;
+  auto load = [&](int ch, int b) {
+    char* st = stage + b * B::BUF;
+    load_a16<C>(st, s16, row0, B::KC * ch, c.tid);
+    if constexpr (YST)
+      load_by16<C>(st + B::ABYTES, v, B::KC * ch, c.C0, c.tid);
+    else
+      load_bx16<C>(st + B::ABYTES, v, c.R0, B::KC * ch, c.tid);
+  };
+  load(0, 0);
+  cp_async_commit();
+  for (int ch = 0; ch < NK; ++ch) {
+    if (ch + 1 < NK) load(ch + 1, (ch + 1) & 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const uint32_t sa = smem_addr(stage + (ch & 1) * B::BUF);
+    const uint32_t sb = sa + B::ABYTES;
+#pragma unroll
+    for (int kk = 0; kk < B::KC; kk += 16) {
+      uint32_t a[4];
+      ldsm_x4(a, sa + 2u * (arow * B::AS + kk + 8 * (q >> 1)));
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        uint32_t b[4];
+        if constexpr (YST)
+          ldsm_x4_t(b, sb + 2u * ((kk + r + 8 * (q & 1)) * B::BYS + 16 * c.wc0 + 8 * (2 * p + (q >> 1))));
+        else
+          ldsm_x4(b, sb + 2u * ((16 * c.wc0 + 8 * (2 * p + (q >> 1)) + r) * B::AS + kk + 8 * (q & 1)));
+        hmma_f16(acc[2 * p], a, b[0], b[1]);
+        hmma_f16(acc[2 * p + 1], a, b[2], b[3]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Group maximum of a nonnegative value (one barrier; channel 3 of the reduction slots).
+template <class C>
+__device__ __forceinline__ double big_max(double m, double* wred, BigSync<C>& sy, int buf, const BigCtx& c) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if (c.lane == 0) wred[3 * 64 + c.warp] = m;
+  __syncthreads();
+  if (c.warp == 0) {
+    double x = c.lane < C::WARPS ? wred[3 * 64 + c.lane] : 0.0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, off));
+    if constexpr (C::GSYNC) {
+      if (c.lane == 0) sy.gred[(buf * 4 + 3) * C::G + c.rank] = x;
+    } else {
+      if (c.lane < C::G) sy.tred_peer[c.lane][buf * 4 * 16 + 3 * 16 + c.rank] = x;
+    }
+  }
+  big_sync<C>(sy);
+  double x = 0.0;
+  if constexpr (C::GSYNC) {
+    const double* g = sy.gred + (buf * 4 + 3) * C::G;
+#pragma unroll
+    for (int q = 0; q < C::G; q += 32)
+      if (q + c.lane < C::G) x = fmax(x, __ldcg(g + q + c.lane));
+  } else {
+    x = c.lane < C::G ? sy.tred[buf * 4 * 16 + 3 * 16 + c.lane] : 0.0;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, off));
+  return x;
+}
+
 template <class C, bool PRE>
 __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
   extern __shared__ __align__(16) double smem[];
@@ -526,6 +656,8 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
 
   int buf = 0;
   double acc[8][4];
+  const bool lp_dst = PRE && W.precond == 2 && P.dst16 != nullptr;  // FP16 DST stages
+  double lp_dbound = 1.0;
 
   auto put_tile = [&](double* pv, int j, int i, double v) { pv[pv_idx<C>(j, i)] = v; };
 
@@ -548,6 +680,10 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
     bool in_tile = false;
     for (int n = n0; n <= n1; ++n) {
       const double s = 0.5 * W.d_dt[n - 1];
+      if (lp_dst) {
+        const double dlow = P.lp_dmin + s * P.lp_kmin;
+        lp_dbound = dlow > 0.0 ? 1.0 / dlow : 0.0;  // >= max 1/d(s) (FP16 stage scaling)
+      }
       const double fs = W.d_f ? (W.d_fscale ? W.d_fscale[n] : 1.0) : 0.0;
       const double* Fn = W.d_f ? W.d_f + (int64_t)n * W.f_stride : nullptr;
       int64_t nmv = need_in ? 1 : 0, npc = 0;
@@ -693,6 +829,63 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
         }
         ++npc;
       };
+      // FP16 DST stages (precond 2): V16a <- r s1; V16b <- x-stage; V16a <- y-stage * dinv s2; V16b <- x-stage;
+      // acc <- y-stage / (s1 s2)
+      auto apply_tau_big_lp = [&]() {
+        using BL = BigLp<C>;
+        uint16_t* v16a = reinterpret_cast<uint16_t*>(pv1);
+        uint16_t* v16b = v16a + (size_t)C::NP * BL::SHH;
+        char* st16 = reinterpret_cast<char*>(stage);
+        __syncthreads();
+        double m = 0.0;
+        RM_BIG_FOR { m = fmax(m, fabs(__ldcg(rs + big_fidx(c, nf, e)))); }
+        // (its group barrier also orders every CTA's last read of pv1 before the writes below)
+        const double gm = big_max<C>(m, wred, sy, buf, c);
+        const int e1 = gm > 0.0 ? 6 - ilogb(gm) : 0;
+        const int e2 = lp_dbound > 0.0 ? -ilogb(lp_dbound) : 0;
+        const double s1 = ldexp(1.0, e1), s2 = ldexp(1.0, e2), unscale = ldexp(1.0, -e1 - e2);
+#pragma unroll
+        for (int nf = 0; nf < 8; ++nf)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int j = big_row(c, 2 * h), i = big_col(c, nf, 2 * h);
+            const bool in = j < ny;
+            const float lo = (in && i < nx) ? (float)(__ldcg(rs + big_fidx(c, nf, 2 * h)) * s1) : 0.f;
+            const float hi = (in && i + 1 < nx) ? (float)(__ldcg(rs + big_fidx(c, nf, 2 * h + 1)) * s1) : 0.f;
+            *reinterpret_cast<uint32_t*>(v16a + (size_t)j * BL::SHH + i) = pack_f16x2(lo, hi);
+          }
+        big_sync<C>(sy);
+        float a32[8][4];
+#pragma unroll 1
+        for (int pass = 0; pass < 2; ++pass) {
+          big_dst16<C, false>(P.dst16, v16a, st16, a32, c);
+          RM_BIG_FOR {
+            const int j = c.R0 + 16 * c.wc0 + 8 * nf + 2 * c.tig + (e & 1);
+            const int i = c.C0 + 16 * c.wr + c.gq + 8 * (e >> 1);
+            v16b[(size_t)j * BL::SHH + i] = to_f16(a32[nf][e]);
+          }
+          big_sync<C>(sy);
+          big_dst16<C, true>(P.dst16, v16b, st16, a32, c);
+          if (pass == 1) break;
+          // every CTA finished its x-stage reads of V16a before the barrier above
+#pragma unroll
+          for (int nf = 0; nf < 8; ++nf)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int j = big_row(c, 2 * h), i = big_col(c, nf, 2 * h);
+              const bool in = j < ny;
+              const float lo =
+                  (in && i < nx) ? (float)(a32[nf][2 * h] * (__ldcg(ds + big_fidx(c, nf, 2 * h)) * s2)) : 0.f;
+              const float hi =
+                  (in && i + 1 < nx) ? (float)(a32[nf][2 * h + 1] * (__ldcg(ds + big_fidx(c, nf, 2 * h + 1)) * s2))
+                                     : 0.f;
+              *reinterpret_cast<uint32_t*>(v16a + (size_t)j * BL::SHH + i) = pack_f16x2(lo, hi);
+            }
+          big_sync<C>(sy);
+        }
+        RM_BIG_FOR { acc[nf][e] = (double)a32[nf][e] * unscale; }
+        ++npc;
+      };
       auto set_direction_from = [&](bool use_z) {
         // p = z (PRE) or r into pv0 (after every CTA finished reading pv0)
         big_sync<C>(sy);
@@ -705,7 +898,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
 
       if (!done) {
         if constexpr (PRE) {
-          apply_tau_big();
+          if (lp_dst) apply_tau_big_lp(); else apply_tau_big();
           double p1[1][4] = {{0, 0, 0, 0}};
           RM_BIG_FOR { p1[0][nf >> 1] += __ldcg(rs + big_fidx(c, nf, e)) * acc[nf][e]; }
           double rz[1];
@@ -774,7 +967,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
         }
         double red2[2];
         if constexpr (PRE) {
-          apply_tau_big();
+          if (lp_dst) apply_tau_big_lp(); else apply_tau_big();
           RM_BIG_FOR { part2[1][nf >> 1] += __ldcg(rs + big_fidx(c, nf, e)) * acc[nf][e]; }
           big_reduce<C, 2>(part2, wred, sy, buf, c, red2);
         } else {
@@ -825,7 +1018,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
             break;
           }
           if constexpr (PRE) {
-            apply_tau_big();
+            if (lp_dst) apply_tau_big_lp(); else apply_tau_big();
             double p3[1][4] = {{0, 0, 0, 0}};
             RM_BIG_FOR { p3[0][nf >> 1] += __ldcg(rs + big_fidx(c, nf, e)) * acc[nf][e]; }
             double rz[1];

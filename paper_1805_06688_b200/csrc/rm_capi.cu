@@ -289,9 +289,12 @@ int rm_sweep_run(rm_grid* g, const rm_sweep* sw, void* stream) {
     a.gbar = g->d_gbar;
     a.gbuf = g->d_gbuf;
     a.sw = *sw;
-    if (a.sw.precond == 2) a.sw.precond = 1;  // the large-grid kernel runs its DST stages in FP64 (for now)
-    a.dst16 = nullptr;
-    a.lp_dmin = a.lp_kmin = a.gen_absmax = 0.0;
+    // FP16 DST stages for square grids; the split-FP16 iteration applies are a small-grid feature
+    a.dst16 = g->d_dst16;
+    if (a.sw.precond == 2 && !g->d_dst16) a.sw.precond = 1;
+    a.lp_dmin = g->lp_dmin;
+    a.lp_kmin = g->lp_kmin;
+    a.gen_absmax = g->gen_absmax;
     a.sw.lp_matvec = 0;
     a.nx = g->nx;
     a.ny = g->ny;
@@ -381,7 +384,7 @@ int rm_grid_set_tau(rm_grid* g, const double* dm, const double* dk) {
     g->lp_dmin = std::min(g->lp_dmin, dm[i]);
     g->lp_kmin = std::min(g->lp_kmin, dk[i]);
   }
-  if (!rm::big_supported(np) && g->nx == g->ny) {
+  if (g->nx == g->ny) {
     // FP16 DST-I matrix for the low-precision stages: row alpha-1, column kappa-1, zero beyond n
     // (rm_device.cuh Lp); |S| <= sqrt(2/(n+1)) and every nonzero entry is an FP16 normal number
     const int sh = np + 8, nn = g->nx;

@@ -19,6 +19,7 @@ ap.add_argument("--config", default="cfg3")
 ap.add_argument("--chains", type=int, nargs="+", default=[37, 148])
 ap.add_argument("--steps", type=int, default=7)
 ap.add_argument("--dt", type=float, default=None)
+ap.add_argument("--precond", default="tau")
 a = ap.parse_args()
 case = make_case(a.config, Nt=8)
 eng = Engine.for_problem(case.grid, case.beta, case.gamma, case.kx, case.ky)
@@ -37,11 +38,11 @@ for nch in a.chains:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         eng.sweep(nchains=nch, first=1, cstride=m, clen=m - 1, nmax=N, dt=dt, counters=cnt, rel_tol=1e-12,
-                  src=V, x0_mode=1, gadd=G_, out=V, precond="tau")
+                  src=V, x0_mode=1, gadd=G_, out=V, precond=a.precond)
         e1.record()
         torch.cuda.synchronize()
         c = cnt.cpu().tolist()
         ms = e0.elapsed_time(e1)
         tf = (c[2] * F + c[3] * FP) / (ms * 1e-3) / 1e12
-        print(f"{a.config} chains={nch} steps={m - 1}: {ms:8.2f} ms, {c[1] / max(c[0], 1):.1f} its/solve, "
+        print(f"{a.config} {a.precond} chains={nch} steps={m - 1}: {ms:8.2f} ms, {c[1] / max(c[0], 1):.1f} its/solve, "
               f"{c[2]} applies, {c[3]} precond -> {tf:.2f} TF/s", flush=True)
