@@ -303,19 +303,18 @@ def run_ours(args):
     mvs = sum(int((after - before)[2].item()) for _, _, _, before, after, _ in trace)
     pcs = sum(int((after - before)[3].item()) for _, _, _, before, after, _ in trace)
     mvs16 = sum(int((after - before)[4].item()) for _, _, _, before, after, _ in trace)
-    # the chain kernel mixes FP64 DMMA (operator applies) with FP16 HMMA (tau DST stages, 'tau'):
-    # its time bound is F64 / P64 + F16 / P16, so the roofline peak is the FLOP-weighted harmonic mean
-    # of the two measured peaks and frac = bound / measured time
-    f64 = mvs * fmv(case.grid.nx, case.grid.ny, eng.flags)
-    lp = args.precond in ("tau", "tau16") and case.grid.nx == case.grid.ny  # FP16 DST stages: square grids
-    if lp:
-        f16 = pcs * fpc_dense(case.grid.nx, case.grid.ny) + mvs16 * fmv_split16(case.grid.nx, case.grid.ny)
-    else:
-        f64 += pcs * fpc(case.grid.nx, case.grid.ny)
-        f16 = 0.0
+    # Algorithmic FLOPs: F_mv per operator apply -- whether it ran on FP64 DMMA or as a
+    # split-FP16 product inside the PCG iteration -- and F_pc per tau application.  The roofline is the
+    # FP64 tensor peak (the arithmetic the path is specified in); the chain kernel executes part of that
+    # work on FP16 tensor cores, which the auxiliary "executed" fields account for separately: its
+    # executed-FLOP time bound is F64/P64 + F16/P16 (mixed_bound_frac = bound / measured time).
+    nx_, ny_ = case.grid.nx, case.grid.ny
+    alg = (mvs + mvs16) * fmv(nx_, ny_, eng.flags) + pcs * fpc(nx_, ny_)
+    achieved = alg / (k_ms * 1e-3) / 1e12
+    lp = args.precond in ("tau", "tau16") and nx_ == ny_  # FP16 DST stages: square grids
+    f64 = mvs * fmv(nx_, ny_, eng.flags) + (0.0 if lp else pcs * fpc(nx_, ny_))
+    f16 = (pcs * fpc_dense(nx_, ny_) if lp else 0.0) + mvs16 * fmv_split16(nx_, ny_)
     t_bound = f64 / (peak * 1e12) + f16 / (FP16_MMA_SYNC_PEAK_TFLOPS * 1e12)
-    peak_mixed = (f64 + f16) / t_bound / 1e12
-    achieved = (f64 + f16) / (k_ms * 1e-3) / 1e12
     traffic, traffic_launch = ncu_traffic()
 
     # end to end through the public API (host inputs, host result)
@@ -359,24 +358,25 @@ def run_ours(args):
             "e2e": {"value": work / (e2e * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches // args.steps,
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_mixed, "unit": "TFLOP/s",
-                         "frac": achieved / peak_mixed, "traffic": traffic,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": traffic,
                          "kernel": "chain_kernel (fused PCG: FP64 DMMA block-Toeplitz applies for right-hand "
                                    "sides and true residuals, split-FP16 HMMA applies inside the iteration, tau "
                                    "DST stages on FP16 HMMA)",
-                         "peak_source": "FLOP-weighted harmonic mean of the FP64 peak (cuBLAS DGEMM 8192^3 "
-                                        "measured in this run; FP64 is not in MEASURED_PEAKS.json) and the legacy "
-                                        "mma.sync FP16 peak (tools/lowp_peak.cu, profiles/r01_lowp_peak.txt)",
-                         "fp64_peak": peak, "fp16_peak": FP16_MMA_SYNC_PEAK_TFLOPS,
-                         "fp64_flops_per_step": f64, "fp16_flops_per_step": f16,
-                         "fp64_achieved_over_kernel_time": f64 / (k_ms * 1e-3) / 1e12,
+                         "achieved_counts": "algorithmic FP64-equivalent FLOPs: F_mv per operator apply (FP64 or "
+                                            "split-FP16), F_pc per tau application (flops.py)",
+                         "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (FP64 is not in "
+                                        "MEASURED_PEAKS.json)",
+                         "executed_fp64_flops_per_step": f64, "executed_fp16_flops_per_step": f16,
+                         "fp16_peak": FP16_MMA_SYNC_PEAK_TFLOPS,
+                         "fp16_peak_source": "legacy mma.sync FP16 (tools/lowp_peak.cu, profiles/r01_lowp_peak.txt)",
+                         "mixed_bound_frac": t_bound / (k_ms * 1e-3),
                          "traffic_launch": traffic_launch,
-                         "flops_per_apply": fmv(case.grid.nx, case.grid.ny, eng.flags), "applies_per_step": mvs,
-                         "flops_per_precond": fpc_dense(case.grid.nx, case.grid.ny) if lp
-                         else fpc(case.grid.nx, case.grid.ny),
+                         "flops_per_apply": fmv(case.grid.nx, case.grid.ny, eng.flags), "fp64_applies_per_step": mvs,
+                         "flops_per_precond": fpc(case.grid.nx, case.grid.ny),
                          "precond_applies_per_step": pcs,
                          "split_fp16_applies_per_step": mvs16,
-                         "flops_per_split_fp16_apply": fmv_split16(case.grid.nx, case.grid.ny),
+                         "executed_flops_per_split_fp16_apply": fmv_split16(case.grid.nx, case.grid.ny),
                          "kernel_ms_per_step": k_ms},
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,
