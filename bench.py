@@ -48,8 +48,14 @@ def dist_env():
 
 
 def load_case(args):
+    """The bench workload.  Weak scaling (default): BASELINE config 2's 4096 fine steps PER GPU, i.e. the
+    time horizon grows with the GPU count (Nt = 4096 N, T = N) -- time-parallel MGRIT's use case: each
+    rank owns one cfg2-sized slab.  Strong scaling: the cfg2 problem split over the ranks."""
     from paper_1805_06688_b200.configs import make_case
 
+    ws = dist_env()[0]
+    if args.nt is None and ws > 1 and args.scaling == "weak":
+        return make_case(args.config, Nt=make_case(args.config).tmesh.n_intervals * ws, T=float(ws))
     return make_case(args.config, Nt=args.nt)
 
 
@@ -61,7 +67,9 @@ def case_options(case, args):
 
 
 def workload(case):
-    return {"workload": f"BASELINE configs[1] ({case.name}): Riesz SFDE, {case.grid.nx}x{case.grid.ny} DOF, "
+    T = float(case.tmesh.points[-1])
+    per = f" (weak scaling: {int(round(T))} x the BASELINE horizon, T = {T:g}, same step)" if T != 1.0 else ""
+    return {"workload": f"BASELINE configs[1] ({case.name}){per}: Riesz SFDE, {case.grid.nx}x{case.grid.ny} DOF, "
                         f"Nt={case.tmesh.n_intervals} uniform, beta={case.beta}, gamma={case.gamma}, "
                         f"Kx={case.kx}, Ky={case.ky}, multilevel MGRIT V-cycle m={case.m} FCF, CG tol "
                         f"{case.cg_rel_tol:g}, halt {case.halt_tol:g}",
@@ -127,11 +135,21 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- CPU reference leg
 def reference_counts(case):
+    """Reference-equivalent solve / CG counts of cfg2 (Nt = 4096); for the weak-scaled Nt = 4096 k the
+    counts are scaled by k (solve counts grow linearly with Nt at a fixed MGRIT iteration count; the
+    extra coarse level is not charged) and labelled as such."""
     path = os.path.join(PROFILES, f"{case.name}_reference_counts.json")
-    if case.name == "cfg2" and case.tmesh.n_intervals == 4096 and os.path.exists(path):
-        with open(path) as f:
-            return json.load(f)
-    return None
+    n = case.tmesh.n_intervals
+    if case.name != "cfg2" or n % 4096 or not os.path.exists(path):
+        return None
+    with open(path) as f:
+        counts = json.load(f)
+    k = n // 4096
+    if k > 1:
+        scale = lambda d: {key: v * k for key, v in d.items()}  # noqa: E731
+        counts = dict(counts, setup=scale(counts["setup"]), levels=[scale(d) for d in counts["levels"]],
+                      source=counts["source"] + f"; scaled x{k} for Nt = {n} (weak scaling)")
+    return counts
 
 
 def cpu_sample(case, counts, budget_s: float = 12.0):
@@ -161,6 +179,8 @@ def cpu_sample(case, counts, budget_s: float = 12.0):
             applies += (st.cg_its - its0) + 3  # explicit + initial residual + CG iterations + true residual
             nprop += 1
         t_apply = (time.perf_counter() - t0) / applies
+        if li >= len(counts["levels"]):
+            break  # weak-scaled runs have one more (tiny) coarse level than the counted cfg2 run
         c = counts["levels"][li]
         est += t_apply * (c["cg_iterations"] + 3 * c["solves"])
         if li == 0:
@@ -202,7 +222,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": tts * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (canonical seeded recipe)",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic (canonical seeded recipe)",
         "config": workload(case),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
                          "sample_wall_s": statistics.median(t_run), "extrapolated_tts_s": tts},
@@ -350,7 +370,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (canonical seeded recipe, SURVEY.md §8d)",
             "config": dict(workload(case), mgrit_iterations=iters, cg_preconditioner=args.precond,
                            parallelism=(f"time slabs x{ws} (contiguous coarse intervals per rank, NCCL C-point "
@@ -391,6 +411,8 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="N > 1: weak = 4096 fine steps of cfg2 per GPU (default), strong = cfg2 split over GPUs")
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")

@@ -69,8 +69,9 @@ CONFIGS = {
 
 
 def make_case(name: str, M: int | None = None, Nt: int | None = None,
-              max_levels: int | None | str = "default") -> CaseSpec:
-    """Build a configuration; ``M``/``Nt`` override the sizes (reduced parity cases)."""
+              max_levels: int | None | str = "default", T: float = 1.0) -> CaseSpec:
+    """Build a configuration; ``M``/``Nt`` override the sizes (reduced parity cases); ``T`` the final time
+    (BASELINE: T = 1; bench.py's weak scaling extends the horizon at a fixed step, T = Nt / Nt_config)."""
     M0, Nt0, beta, gamma, kx, ky, m, lv = CONFIGS[name]
     M = M0 if M is None else M
     Nt = Nt0 if Nt is None else Nt
@@ -80,7 +81,7 @@ def make_case(name: str, M: int | None = None, Nt: int | None = None,
     x, y = grid.interior_nodes()
     n = grid.ndof
     sxy = np.sin(np.pi * x) * np.sin(np.pi * y)
-    tmesh = uniform_temporal(1.0, Nt)
+    tmesh = uniform_temporal(T, Nt)
     if name == "cfg1":
         rng = np.random.default_rng(0)
         psi0 = x * (1 - x) * y * (1 - y) * (1.0 + 0.01 * rng.standard_normal(n))
@@ -104,7 +105,7 @@ def make_case(name: str, M: int | None = None, Nt: int | None = None,
         psi0 = sxy + 1e-3 * np.random.default_rng(1).standard_normal(n)
         g = np.random.default_rng(0).uniform(-1.0, 1.0, n)
         kind = "exp_neg_t"
-        tmesh = graded_temporal(1.0, Nt, 2.0)
+        tmesh = graded_temporal(T, Nt, 2.0)
     elif name == "cfg5":
         rng = np.random.default_rng(0)
         psi0 = sxy.copy()
