@@ -224,3 +224,18 @@ def test_trace_payload_schema(tmp_path):
     text = out.read_text()
     assert text.endswith("\n") and json.loads(text) == json.loads(json.dumps(p | {"config": {"b": 1, "a": 2}}))
     assert text.index('"cg_iterations"') < text.index('"config"')  # sort_keys=True
+
+
+def test_preconditioner_names_and_options():
+    """CgOptions / MgritOptions accept the inner-solver variants (krylov.py:12-20 plus the extensions) and
+    reject anything else with ValueError, as the reference validates its options."""
+    from paper_1805_06688_b200.krylov import CgOptions
+    from paper_1805_06688_b200.mgrit import MgritOptions
+
+    for name in ("tau", "tau16", "tau64", "none"):
+        assert CgOptions(preconditioner=name).preconditioner == name
+        assert MgritOptions(m=4, cg_preconditioner=name).cg_preconditioner == name
+    with pytest.raises(ValueError):
+        CgOptions(preconditioner="jacobi")
+    with pytest.raises(ValueError):
+        CgOptions(rel_tol=0.0)
