@@ -154,6 +154,12 @@ typedef struct rm_sweep {
      split-FP16 tensor-core product (~2^-22 relative; rm_device.cuh Mx), every stopping decision still on
      the FP64 true residual; grids 63^2 .. 127^2 (others ignore the flag).  0: FP64 throughout. */
   int lp_matvec;
+  /* optional (explicit_rhs chains): rows n = (M + dt_n/2 K) G_n, dt_n = d_dt[n-1], of the G added in the
+     epilogue (d_gadd; zero rows if none).  Inside a chain the next step's explicit side then follows from
+     the accepted solve without an operator apply (the step's input is y = x + G):
+       (M - s K) y = (1 + s/s0) M y - (s/s0) (b - r + (M + s0 K) G).   NULL: apply as usual. */
+  const double* d_hg;
+  int64_t hg_stride;
 } rm_sweep;
 
 RM_API int rm_sweep_run(rm_grid* grid, const rm_sweep* sweep, void* stream);

@@ -580,7 +580,9 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
 
     const int n0 = W.first + chain * W.cstride;
     const int n1 = min(n0 + W.clen - 1, W.nmax);
-    bool in_tile = false;  // previous step left this step's input in Vt
+    bool in_tile = false;   // previous step left this step's input in Vt
+    bool chain_ok = false;  // ... and its accepted true residual in rr_ (apply-free next right-hand side)
+    double s_prev = 0.0;
     for (int n = n0; n <= n1; ++n) {
       const double s = 0.5 * W.d_dt[n - 1];
       if (lp_dst) {
@@ -600,13 +602,35 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
 
       // ---------------- right-hand side, initial iterate and residual --------------
       // (the previous step ended with a group barrier: nobody reads the tables any more)
-      if (need_in) {
+      // Inside a chain (the previous step's output y_{n-1} = x + G_{n-1} is in the tile and its true residual
+      // r = b - A_{s0} x in rr_) the explicit side needs no apply:
+      //   (M - s K) y = (1 + s/s0) M y - (s/s0) (b - r + A_{s0} G_{n-1}),   A_{s0} G_{n-1} = d_hg row n-1
+      // (host-precomputed per level; s0 = dt_{n-1}/2).  Exact up to rounding.
+      const bool rhs_free = need_in && W.explicit_rhs && in_tile && chain_ok && W.d_hg != nullptr &&
+                            W.d_gadd != nullptr && W.d_sub == nullptr;
+      if (need_in && !rhs_free) {
         build_step_tables<C::NP, C::GL, C::THREADS>(gens, P.gens, -s, cm, c.tid);  // M - s K
         if (!in_tile) load_vec<C>(Vt, W.d_src + (int64_t)(n - 1) * W.src_stride, nx, ny, c);
         __syncthreads();
         matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true, P.merge);
       }
-      int64_t nmv = need_in ? 1 : 0;
+      if (rhs_free) {
+        __syncthreads();  // the tile's halo (re-zeroed above in the split-FP16 mode) before the mass stencil
+        const double* Hn = W.d_hg + (int64_t)(n - 1) * W.hg_stride;
+        const double q = s / s_prev;
+        RM_FOR_ELEM {
+          const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
+          double am = 0.0;
+          if (j < ny && i < nx) {
+            const double ax = sb_[elem_sidx<C>(c, mr, nf, e)] - rr_[mr][nf][e] + __ldcg(Hn + j * nx + i);
+            am = (1.0 + q) * mass_stencil<C>(Vt, j, i, cm) - q * ax;
+          }
+          acc[mr][nf][e] = am;
+        }
+      }
+      s_prev = s;
+      chain_ok = false;  // set again when this step's solve is accepted
+      int64_t nmv = need_in && !rhs_free ? 1 : 0;
       int64_t nmv16 = 0;  // split-FP16 applies (lp_step)
       int64_t npc = 0;  // preconditioner applications
       double part[2][C::WR][C::WC];
@@ -953,6 +977,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           const double true_res = sqrt(tt[0]);
           // the reference's acceptance; the split-FP16 iteration accepts only a true residual <= target
           if (true_res <= (lp_step ? target : fmax(target, 10.0 * res))) {
+            RM_FOR_ELEM { rr_[mr][nf][e] = acc[mr][nf][e]; }  // r_n = b_n - A x_n for the chain's next rhs
             its = k;
             done = true;
             break;
@@ -1026,6 +1051,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
         RM_T(6);
       }
 
+      chain_ok = done && !fail && W.x0_mode < 3;
       if (c.rank == 0 && c.tid == 0) {
         atomicAdd(W.d_counters, 1ull);
         atomicAdd(W.d_counters + 1, (unsigned long long)its);

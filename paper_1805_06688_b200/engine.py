@@ -183,7 +183,8 @@ class Engine:
               fscale: torch.Tensor | None = None, gadd: torch.Tensor | None = None, sub: torch.Tensor | None = None,
               out: torch.Tensor | None = None, out_div: int = 1, norms: torch.Tensor | None = None,
               max_iter: int | None = None, group: int = 0, row: int | None = None, tag: str = "",
-              precond: str = "none", guess=None, keep: torch.Tensor | None = None) -> None:
+              precond: str = "none", guess=None, keep: torch.Tensor | None = None,
+              hg: torch.Tensor | None = None) -> None:
         """One rm_sweep_run launch; 2-D arrays are indexed by time point with row stride ``row``."""
         if nchains <= 0:
             return
@@ -204,6 +205,7 @@ class Engine:
         sw.d_norms = _ptr(norms, 1)
         sw.d_guess, sw.guess_stride = _ptr(guess, row), row
         sw.d_keep, sw.keep_stride = _ptr(keep, row), row
+        sw.d_hg, sw.hg_stride = _ptr(hg, row), row
         sw.rel_tol = float(rel_tol)
         sw.max_iter = -1 if max_iter is None else int(max_iter)
         if counters.dtype != torch.int64 or not counters.is_cuda or counters.numel() < 5:
