@@ -160,6 +160,11 @@ typedef struct rm_sweep {
        (M - s K) y = (1 + s/s0) M y - (s/s0) (b - r + (M + s0 K) G).   NULL: apply as usual. */
   const double* d_hg;
   int64_t hg_stride;
+  /* optional: A x = b - r of every accepted solve (r the FP64 true residual) to d_ax[n / out_div]; the
+     setup sweep G_n = A^-1 F_n thereby yields the d_hg rows of the fine level without an apply.  Small-grid
+     kernel (up to 127^2).  NULL: off. */
+  double* d_ax;
+  int64_t ax_stride;
 } rm_sweep;
 
 RM_API int rm_sweep_run(rm_grid* grid, const rm_sweep* sweep, void* stream);

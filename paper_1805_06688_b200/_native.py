@@ -46,6 +46,7 @@ class Sweep(C.Structure):
         ("d_keep", C.c_void_p), ("keep_stride", C.c_int64),
         ("lp_matvec", C.c_int),
         ("d_hg", C.c_void_p), ("hg_stride", C.c_int64),
+        ("d_ax", C.c_void_p), ("ax_stride", C.c_int64),
     ]
 
 

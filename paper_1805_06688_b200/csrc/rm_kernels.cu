@@ -1077,6 +1077,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
       const double* Sn = W.d_sub ? W.d_sub + (int64_t)n * W.sub_stride : nullptr;
       double* On = W.d_out ? W.d_out + (int64_t)oi * W.out_stride : nullptr;
       double* Kn = W.d_keep ? W.d_keep + (int64_t)oi * W.keep_stride : nullptr;
+      double* An = W.d_ax ? W.d_ax + (int64_t)oi * W.ax_stride : nullptr;
       double p1[1][C::WR][C::WC];
       zero_part<C>(p1[0]);
       RM_FOR_ELEM {
@@ -1084,6 +1085,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
         if (j < ny && i < nx) {
           const int gi = j * nx + i;
           double y = xs[elem_xidx<C>(c, mr, nf, e)];
+          if (An) An[gi] = sb_[elem_sidx<C>(c, mr, nf, e)] - rr_[mr][nf][e];  // A x = b - r (true residual)
           if (Gn) y = __ldcg(Gn + gi) + y;
           if (Kn) Kn[gi] = y;
           if (Sn) y = y - __ldcg(Sn + gi);
