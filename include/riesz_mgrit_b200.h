@@ -165,6 +165,11 @@ typedef struct rm_sweep {
      kernel (up to 127^2).  NULL: off. */
   double* d_ax;
   int64_t ax_stride;
+  /* optional (with d_guess): rows n = A x0' for the second guess x0' = guess_n [- G_n], i.e. the d_ax of the
+     accepted solve that last wrote that point with the same operator and G: the guess' initial residual
+     then needs no apply.  NULL: applied. */
+  const double* d_gax;
+  int64_t gax_stride;
 } rm_sweep;
 
 RM_API int rm_sweep_run(rm_grid* grid, const rm_sweep* sweep, void* stream);

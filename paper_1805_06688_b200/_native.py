@@ -47,6 +47,7 @@ class Sweep(C.Structure):
         ("lp_matvec", C.c_int),
         ("d_hg", C.c_void_p), ("hg_stride", C.c_int64),
         ("d_ax", C.c_void_p), ("ax_stride", C.c_int64),
+        ("d_gax", C.c_void_p), ("gax_stride", C.c_int64),
     ]
 
 

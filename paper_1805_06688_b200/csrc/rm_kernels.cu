@@ -693,17 +693,23 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
         // second candidate start x0' = guess_n [- G_n] (the value this solve is about to replace);
         // keep whichever initial residual is smaller (deterministic: both norms are group-reduced)
         const double* Gr = W.d_gadd ? W.d_gadd + (int64_t)n * W.gadd_stride : nullptr;
-        load_guess<C>(Vt, W.d_guess + (int64_t)n * W.guess_stride, Gr, nx, ny, c);
-        __syncthreads();
-        matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true, P.merge);
-        ++nmv;
+        const double* Gu = W.d_guess + (int64_t)n * W.guess_stride;
+        // A x0' is either applied, or -- when this point was last written by an accepted solve of the same
+        // operator whose A x was stored (d_gax) -- read back: no apply
+        const double* Ax0 = W.d_gax ? W.d_gax + (int64_t)n * W.gax_stride : nullptr;
+        if (!Ax0) {
+          load_guess<C>(Vt, Gu, Gr, nx, ny, c);
+          __syncthreads();
+          matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true, P.merge);
+          ++nmv;
+        }
         double pg[1][C::WR][C::WC];
         zero_part<C>(pg[0]);
         RM_FOR_ELEM {
           const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
           double r = 0.0;
           if (j < ny && i < nx)
-            r = sb_[elem_sidx<C>(c, mr, nf, e)] - acc[mr][nf][e];
+            r = sb_[elem_sidx<C>(c, mr, nf, e)] - (Ax0 ? __ldcg(Ax0 + j * nx + i) : acc[mr][nf][e]);
           acc[mr][nf][e] = r;
           pg[0][mr][nf >> 1] += r * r;
         }
@@ -714,7 +720,14 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           tot[1] = rg[0];
           RM_FOR_ELEM {
             const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
-            xs[elem_xidx<C>(c, mr, nf, e)] = (j < ny && i < nx) ? Vt[vt_idx<C>(j, i)] : 0.0;
+            double x0 = 0.0;
+            if (j < ny && i < nx) {
+              if (Ax0)
+                x0 = Gr ? __ldcg(Gu + j * nx + i) - __ldcg(Gr + j * nx + i) : __ldcg(Gu + j * nx + i);
+              else
+                x0 = Vt[vt_idx<C>(j, i)];
+            }
+            xs[elem_xidx<C>(c, mr, nf, e)] = x0;
             rr_[mr][nf][e] = acc[mr][nf][e];
           }
         }
