@@ -821,6 +821,9 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
         pf(W.d_gadd, W.gadd_stride);
         pf(W.d_f, W.f_stride);
         pf(W.d_sub, W.sub_stride);
+        pf(W.d_gax, W.gax_stride);
+        if (W.d_hg)  // the next step's apply-free right-hand side reads row n
+          prefetch_l2(reinterpret_cast<const char*>(W.d_hg + (int64_t)n * W.hg_stride) + lo, hi - lo);
       }
       RM_T0();
       for (int64_t k = 1; !done; ++k) {
