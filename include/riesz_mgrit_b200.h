@@ -161,8 +161,7 @@ typedef struct rm_sweep {
   const double* d_hg;
   int64_t hg_stride;
   /* optional: A x = b - r of every accepted solve (r the FP64 true residual) to d_ax[n / out_div]; the
-     setup sweep G_n = A^-1 F_n thereby yields the d_hg rows of the fine level without an apply.  Small-grid
-     kernel (up to 127^2).  NULL: off. */
+     setup sweep G_n = A^-1 F_n thereby yields the d_hg rows of the fine level without an apply.  NULL: off. */
   double* d_ax;
   int64_t ax_stride;
   /* optional (with d_guess): rows n = A x0' for the second guess x0' = guess_n [- G_n], i.e. the d_ax of the

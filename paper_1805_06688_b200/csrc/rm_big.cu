@@ -678,6 +678,8 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
     const int n0 = W.first + chain * W.cstride;
     const int n1 = min(n0 + W.clen - 1, W.nmax);
     bool in_tile = false;
+    bool chain_ok = false;  // the previous step's accepted true residual is in rs (apply-free next rhs)
+    double s_prev = 0.0;
     for (int n = n0; n <= n1; ++n) {
       const double s = 0.5 * W.d_dt[n - 1];
       if (lp_dst) {
@@ -686,9 +688,27 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
       }
       const double fs = W.d_f ? (W.d_fscale ? W.d_fscale[n] : 1.0) : 0.0;
       const double* Fn = W.d_f ? W.d_f + (int64_t)n * W.f_stride : nullptr;
-      int64_t nmv = need_in ? 1 : 0, npc = 0;
+      // apply-free explicit side inside a chain (see the small-grid kernel):
+      //   (M - s K) y = (1 + s/s0) M y - (s/s0) (b - r + A_{s0} G_{n-1})
+      const bool rhs_free = need_in && W.explicit_rhs && in_tile && chain_ok && W.d_hg != nullptr &&
+                            W.d_gadd != nullptr && W.d_sub == nullptr;
+      int64_t nmv = need_in && !rhs_free ? 1 : 0, npc = 0;
+      if (rhs_free) {
+        const double* Hn = W.d_hg + (int64_t)(n - 1) * W.hg_stride;
+        const double q = s / s_prev;
+        RM_BIG_FOR {
+          const int j = big_row(c, e), i = big_col(c, nf, e);
+          const int fi = big_fidx(c, nf, e);
+          double am = 0.0;
+          if (j < ny && i < nx)
+            am = (1.0 + q) * big_mass<C>(pv0, j, i, cm) - q * (bs[fi] - rs[fi] + __ldcg(Hn + j * nx + i));
+          acc[nf][e] = am;
+        }
+      }
+      s_prev = s;
+      chain_ok = false;
 
-      if (need_in) {
+      if (need_in && !rhs_free) {
         // step-operator tables M - s K (rm_device.cuh build_step_tables); the previous step ended
         // with a group barrier
         build_step_tables<C::NP, C::GL, C::THREADS>(gens, P.gens, -s, cm, c.tid);
@@ -765,21 +785,26 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
       if (W.d_guess && sqrt(tot[1]) > target) {
         const double* gu = W.d_guess + (int64_t)n * W.guess_stride;
         const double* Gr = W.d_gadd ? W.d_gadd + (int64_t)n * W.gadd_stride : nullptr;
-        RM_BIG_FOR {
-          const int j = big_row(c, e), i = big_col(c, nf, e);
-          if (j < ny && i < nx) {
-            const int gi = j * nx + i;
-            put_tile(pv0, j, i, Gr ? __ldcg(gu + gi) - __ldcg(Gr + gi) : __ldcg(gu + gi));
+        // A x0' applied, or read back from the solve that wrote the point (d_gax, see the small kernel)
+        const double* Ax0 = W.d_gax ? W.d_gax + (int64_t)n * W.gax_stride : nullptr;
+        if (!Ax0) {
+          RM_BIG_FOR {
+            const int j = big_row(c, e), i = big_col(c, nf, e);
+            if (j < ny && i < nx) {
+              const int gi = j * nx + i;
+              put_tile(pv0, j, i, Gr ? __ldcg(gu + gi) - __ldcg(Gr + gi) : __ldcg(gu + gi));
+            }
           }
+          big_sync<C>(sy);
+          big_matvec<C>(pv0, gens, stage, acc, c, kx_end, ky_end, P.merge);
+          ++nmv;
         }
-        big_sync<C>(sy);
-        big_matvec<C>(pv0, gens, stage, acc, c, kx_end, ky_end, P.merge);
-        ++nmv;
         double pg[1][4] = {{0, 0, 0, 0}};
         RM_BIG_FOR {
           const int j = big_row(c, e), i = big_col(c, nf, e);
           double r = 0.0;
-          if (j < ny && i < nx) r = bs[big_fidx(c, nf, e)] - acc[nf][e];
+          if (j < ny && i < nx)
+            r = bs[big_fidx(c, nf, e)] - (Ax0 ? __ldcg(Ax0 + j * nx + i) : acc[nf][e]);
           acc[nf][e] = r;
           pg[0][nf >> 1] += r * r;
         }
@@ -791,7 +816,12 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
           RM_BIG_FOR {
             const int j = big_row(c, e), i = big_col(c, nf, e);
             const int fi = big_fidx(c, nf, e);
-            xs[fi] = (j < ny && i < nx) ? __ldcg(pv0 + pv_idx<C>(j, i)) : 0.0;
+            double x0 = 0.0;
+            if (j < ny && i < nx) {
+              const int gi = j * nx + i;
+              x0 = Ax0 ? (Gr ? __ldcg(gu + gi) - __ldcg(Gr + gi) : __ldcg(gu + gi)) : __ldcg(pv0 + pv_idx<C>(j, i));
+            }
+            xs[fi] = x0;
             rs[fi] = acc[nf][e];
           }
         }
@@ -1006,6 +1036,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
           buf ^= 1;
           const double true_res = sqrt(tt[0]);
           if (true_res <= fmax(target, 10.0 * res)) {
+            RM_BIG_FOR { rs[big_fidx(c, nf, e)] = acc[nf][e]; }  // r = b - A x for the chain's next rhs
             its = k;
             done = true;
             break;
@@ -1047,6 +1078,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
         big_sync<C>(sy);
       }
 
+      chain_ok = done && !fail;
       if (c.rank == 0 && c.tid == 0) {
         atomicAdd(W.d_counters, 1ull);
         atomicAdd(W.d_counters + 1, (unsigned long long)its);
@@ -1069,6 +1101,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
       const double* Sn = W.d_sub ? W.d_sub + (int64_t)n * W.sub_stride : nullptr;
       double* On = W.d_out ? W.d_out + (int64_t)oi * W.out_stride : nullptr;
       double* Kn = W.d_keep ? W.d_keep + (int64_t)oi * W.keep_stride : nullptr;
+      double* An = W.d_ax ? W.d_ax + (int64_t)oi * W.ax_stride : nullptr;
       big_sync<C>(sy);  // every CTA done reading pv0 before it is overwritten with y
       double py[1][4] = {{0, 0, 0, 0}};
       RM_BIG_FOR {
@@ -1076,6 +1109,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
         if (j < ny && i < nx) {
           const int gi = j * nx + i;
           double y = xs[big_fidx(c, nf, e)];
+          if (An) An[gi] = bs[big_fidx(c, nf, e)] - rs[big_fidx(c, nf, e)];  // A x = b - r (true residual)
           if (Gn) y = __ldcg(Gn + gi) + y;
           if (Kn) Kn[gi] = y;
           if (Sn) y = y - __ldcg(Sn + gi);
