@@ -398,3 +398,21 @@ def test_split_fp16_apply_probe(M, cfg):
     for k in range(4):
         print(k, rel(lp[k], ref[k]))
         assert rel(lp[k], ref[k]) <= 1e-5, (k, rel(lp[k], ref[k]))
+
+
+@pytest.mark.parametrize("cfg,M,Nt", [("cfg2", 32, 256), ("cfg2", 128, 64), ("cfg1", None, 64)])
+def test_apply_reuse_matches_applied_path(cfg, M, Nt, monkeypatch):
+    """The apply-free chain right-hand sides and stored-A x second guesses (rm_sweep d_hg / d_ax / d_gax) give the
+    same MGRIT trajectory as applying the operator: identical iteration and solve counts, per-point solutions
+    within the solve tolerance."""
+    case = make_case(cfg, M=M, Nt=Nt)
+    spec = case_spec(case)
+    opts = MgritOptions(m=case.m, max_levels=case.max_levels, halt_tol=case.halt_tol, cg_rel_tol=case.cg_rel_tol)
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("RM_NO_APPLY_REUSE", flag)
+        out[flag] = solve(spec, opts)
+    (U0, t0), (U1, t1) = out["0"], out["1"]
+    assert t0.iterations == t1.iterations
+    assert t0.spatial_solves == t1.spatial_solves
+    assert per_point_rel(U0, U1).max() <= 1e-10
