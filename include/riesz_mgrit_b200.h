@@ -169,6 +169,11 @@ typedef struct rm_sweep {
      then needs no apply.  NULL: applied. */
   const double* d_gax;
   int64_t gax_stride;
+  /* optional (with d_hg): rows n = A x of the accepted solve that wrote input point n (y = x + G): a chain's
+     first explicit side then needs no apply either, (M - s K) y = (1 + s/s0) M y - (s/s0)(A x + A G).
+     NULL: applied. */
+  const double* d_ain;
+  int64_t ain_stride;
 } rm_sweep;
 
 RM_API int rm_sweep_run(rm_grid* grid, const rm_sweep* sweep, void* stream);

@@ -608,11 +608,29 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
       // (host-precomputed per level; s0 = dt_{n-1}/2).  Exact up to rounding.
       const bool rhs_free = need_in && W.explicit_rhs && in_tile && chain_ok && W.d_hg != nullptr &&
                             W.d_gadd != nullptr && W.d_sub == nullptr;
+      // ... and at a chain's first step whose input point n-1 was written by an accepted solve whose A x was
+      // stored (d_ain, with d_hg): A_{s0} y = A x + A G of that point
+      const bool rhs_ain = need_in && W.explicit_rhs && !in_tile && n >= 2 && W.d_ain != nullptr &&
+                           W.d_hg != nullptr;
       if (need_in && !rhs_free) {
-        build_step_tables<C::NP, C::GL, C::THREADS>(gens, P.gens, -s, cm, c.tid);  // M - s K
+        if (!rhs_ain) build_step_tables<C::NP, C::GL, C::THREADS>(gens, P.gens, -s, cm, c.tid);  // M - s K
         if (!in_tile) load_vec<C>(Vt, W.d_src + (int64_t)(n - 1) * W.src_stride, nx, ny, c);
         __syncthreads();
-        matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true, P.merge);
+        if (!rhs_ain) matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true, P.merge);
+      }
+      if (rhs_ain) {
+        const double* An = W.d_ain + (int64_t)(n - 1) * W.ain_stride;
+        const double* Hn = W.d_hg + (int64_t)(n - 1) * W.hg_stride;
+        const double q = s / (0.5 * W.d_dt[n - 2]);
+        RM_FOR_ELEM {
+          const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
+          double am = 0.0;
+          if (j < ny && i < nx) {
+            const int gi = j * nx + i;
+            am = (1.0 + q) * mass_stencil<C>(Vt, j, i, cm) - q * (__ldcg(An + gi) + __ldcg(Hn + gi));
+          }
+          acc[mr][nf][e] = am;
+        }
       }
       if (rhs_free) {
         __syncthreads();  // the tile's halo (re-zeroed above in the split-FP16 mode) before the mass stencil
@@ -630,7 +648,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
       }
       s_prev = s;
       chain_ok = false;  // set again when this step's solve is accepted
-      int64_t nmv = need_in && !rhs_free ? 1 : 0;
+      int64_t nmv = need_in && !rhs_free && !rhs_ain ? 1 : 0;
       int64_t nmv16 = 0;  // split-FP16 applies (lp_step)
       int64_t npc = 0;  // preconditioner applications
       double part[2][C::WR][C::WC];

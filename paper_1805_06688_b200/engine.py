@@ -185,7 +185,7 @@ class Engine:
               max_iter: int | None = None, group: int = 0, row: int | None = None, tag: str = "",
               precond: str = "none", guess=None, keep: torch.Tensor | None = None,
               hg: torch.Tensor | None = None, ax: torch.Tensor | None = None,
-              gax: torch.Tensor | None = None) -> None:
+              gax: torch.Tensor | None = None, ain: torch.Tensor | None = None) -> None:
         """One rm_sweep_run launch; 2-D arrays are indexed by time point with row stride ``row``."""
         if nchains <= 0:
             return
@@ -209,6 +209,7 @@ class Engine:
         sw.d_hg, sw.hg_stride = _ptr(hg, row), row
         sw.d_ax, sw.ax_stride = _ptr(ax, row), row
         sw.d_gax, sw.gax_stride = _ptr(gax, row), row
+        sw.d_ain, sw.ain_stride = _ptr(ain, row), row
         sw.rel_tol = float(rel_tol)
         sw.max_iter = -1 if max_iter is None else int(max_iter)
         if counters.dtype != torch.int64 or not counters.is_cuda or counters.numel() < 5:

@@ -31,7 +31,7 @@ class CpuEngine:
     def sweep(self, *, nchains, first, cstride, clen, nmax, dt, counters, rel_tol, src=None, explicit=True,
               x0_mode=1, x0=None, f=None, f_stride=0, fscale=None, gadd=None, sub=None, out=None, out_div=1,
               norms=None, max_iter=None, group=0, row=None, tag="", precond="none", guess=None, keep=None,
-              hg=None, ax=None, gax=None):
+              hg=None, ax=None, gax=None, ain=None):
         self.launches += 1
         for c in range(nchains):
             n0 = first + c * cstride
