@@ -708,10 +708,14 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
       s_prev = s;
       chain_ok = false;
 
+      // ... and at a chain's first step from the stored A x of its input point (d_ain, see the small kernel)
+      const bool rhs_ain = need_in && W.explicit_rhs && !in_tile && n >= 2 && W.d_ain != nullptr &&
+                           W.d_hg != nullptr;
+      if (rhs_ain) nmv = 0;
       if (need_in && !rhs_free) {
         // step-operator tables M - s K (rm_device.cuh build_step_tables); the previous step ended
         // with a group barrier
-        build_step_tables<C::NP, C::GL, C::THREADS>(gens, P.gens, -s, cm, c.tid);
+        if (!rhs_ain) build_step_tables<C::NP, C::GL, C::THREADS>(gens, P.gens, -s, cm, c.tid);
         if (!in_tile) {
           const double* src = W.d_src + (int64_t)(n - 1) * W.src_stride;
           RM_BIG_FOR {
@@ -722,7 +726,21 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
         } else {
           __syncthreads();
         }
-        big_matvec<C>(pv0, gens, stage, acc, c, kx_end, ky_end, P.merge);
+        if (!rhs_ain) big_matvec<C>(pv0, gens, stage, acc, c, kx_end, ky_end, P.merge);
+      }
+      if (rhs_ain) {
+        const double* An = W.d_ain + (int64_t)(n - 1) * W.ain_stride;
+        const double* Hn = W.d_hg + (int64_t)(n - 1) * W.hg_stride;
+        const double q = s / (0.5 * W.d_dt[n - 2]);
+        RM_BIG_FOR {
+          const int j = big_row(c, e), i = big_col(c, nf, e);
+          double am = 0.0;
+          if (j < ny && i < nx) {
+            const int gi = j * nx + i;
+            am = (1.0 + q) * big_mass<C>(pv0, j, i, cm) - q * (__ldcg(An + gi) + __ldcg(Hn + gi));
+          }
+          acc[nf][e] = am;
+        }
       }
       double part[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
       RM_BIG_FOR {
