@@ -232,6 +232,81 @@ def big_tight():
          **trace_arrays("c4t", tr))
 
 
+def _sketch_matrix(ndof, k=8, seed=1234):
+    """Fixed seeded projection: U @ R gives per-time-point fingerprints whose relative differences
+    track the per-point relative L2 differences (used where storing all rows is too large)."""
+    return np.random.default_rng(seed).standard_normal((ndof, k)) / np.sqrt(ndof)
+
+
+def _run_and_store(fname, tag, case, keep, lv="case", threads_note=""):
+    spec = ref_spec(case)
+    t = time.perf_counter()
+    opts = MgritOptions(m=case.m, max_levels=case.max_levels if lv == "case" else lv,
+                        halt_tol=case.halt_tol, cg_rel_tol=case.cg_rel_tol, rng_seed=0)
+    U, tr = solve(spec, opts)
+    wall = time.perf_counter() - t
+    print(f"{fname} {tag}: {tr.iterations} its in {wall:.1f}s", flush=True)
+    keep = np.array(sorted(set(int(k) for k in keep if 0 <= k <= case.tmesh.n_intervals)))
+    out = {f"{tag}_keep": keep, f"{tag}_U": U[keep], f"{tag}_norms": np.linalg.norm(U, axis=1),
+           f"{tag}_sketch": U @ _sketch_matrix(U.shape[1]), f"{tag}_wall_s": np.array(wall),
+           f"{tag}_its": np.array(tr.iterations)}
+    out.update(trace_arrays(tag, tr))
+    save(fname, **out)
+
+
+def cfg2_full():
+    """BASELINE configs[1] at full size (127^2 x 4096, multilevel m=8): the workload bench.py timed in
+    round 1.  ~3 h on the 8-core build container."""
+    case = make_case("cfg2")
+    N = case.tmesh.n_intervals
+    _run_and_store("cfg2_full.npz", "c2f", case, [0, 1, 7, 8, 9, 511, 512, 2047, 2048, 2049, 4095, 4096])
+
+
+def cfg2_split():
+    """cfg2 grid and physics on the split-FP16 regime of the benched path: T = 1/8, Nt = 512, i.e. the
+    full run's fine dt = 1/4096 and level-1 dt = 1/512 (levels 512/64/8)."""
+    case = make_case("cfg2", Nt=512, T=0.125)
+    _run_and_store("cfg2_split.npz", "c2p", case, [0, 1, 7, 8, 63, 64, 255, 256, 504, 511, 512])
+
+
+def cfg3_split():
+    """cfg3 grid and physics (255^2, m=16) at the full run's step sizes: T = 1/16, Nt = 1024, i.e. fine
+    dt = 1/16384, level-1 dt = 1/1024, level-2 dt = 1/64 (levels 1024/64/4)."""
+    case = make_case("cfg3", Nt=1024, T=1.0 / 16)
+    _run_and_store("cfg3_split.npz", "c3p", case, [0, 1, 15, 16, 17, 255, 256, 511, 512, 1008, 1023, 1024])
+
+
+def cfg4_diverge():
+    """cfg4 physics (beta=0.55, gamma=0.9, graded t_n=(n/Nt)^2, m=8 multilevel) on 63^2 x 512: the reference's
+    own MGRIT residual GROWS every cycle (the re-discretised Crank-Nicolson coarse propagators of the stiff
+    fractional operator amplify the high modes), as it does on the GPU at the full 511^2 x 8192 size.  Four
+    cycles are recorded; the reference raises MgritFailure, whose trace and iterate are stored."""
+    from riesz_mgrit.mgrit import MgritFailure
+
+    case = make_case("cfg4", M=64, Nt=512)
+    spec = ref_spec(case)
+    t = time.perf_counter()
+    opts = MgritOptions(m=case.m, halt_tol=case.halt_tol, cg_rel_tol=case.cg_rel_tol, max_iters=4)
+    try:
+        solve(spec, opts)
+        raise AssertionError("expected MgritFailure")
+    except MgritFailure as exc:
+        tr, U = exc.trace, exc.solution
+    print(f"cfg4_diverge: {tr.iterations} its in {time.perf_counter() - t:.1f}s: {tr.residual_norms}", flush=True)
+    keep = np.array([0, 1, 8, 64, 256, 511, 512])
+    out = {"c4d_keep": keep, "c4d_U": U[keep], "c4d_norms": np.linalg.norm(U, axis=1),
+           "c4d_sketch": U @ _sketch_matrix(U.shape[1])}
+    out.update(trace_arrays("c4d", tr))
+    save("cfg4_diverge.npz", **out)
+
+
+def cfg4_fullnt():
+    """cfg4 physics on its FULL graded time grid (Nt = 8192, t_n = (n/Nt)^2: every fine dt of the BASELINE
+    run, levels 8192/1024/128/16/2) at a reduced 63^2 grid, where MGRIT converges."""
+    case = make_case("cfg4", M=64)
+    _run_and_store("cfg4_fullnt.npz", "c4n", case, [0, 1, 7, 8, 1024, 4095, 4096, 8184, 8191, 8192])
+
+
 def pcg64():
     rng = np.random.default_rng(0)
     st = rng.bit_generator.state["state"]
@@ -247,7 +322,9 @@ if __name__ == "__main__":
     which = sys.argv[1:] or ["operators", "cg", "stepper", "mgrit_small", "pcg64", "cfg1", "reduced"]
     fns = {"operators": operators, "cg": cg_cases, "stepper": stepper_cases, "mgrit_small": mgrit_small,
            "pcg64": pcg64, "cfg1": cfg1, "reduced": reduced, "big": big,
-           "big_tight": big_tight}
+           "big_tight": big_tight, "cfg2_full": cfg2_full, "cfg2_split": cfg2_split,
+           "cfg3_split": cfg3_split, "cfg4_diverge": cfg4_diverge,
+           "cfg4_fullnt": cfg4_fullnt}
     for w in which:
         t = time.perf_counter()
         fns[w]()
