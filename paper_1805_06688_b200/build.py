@@ -20,7 +20,7 @@ REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIBNAME = "libriesz_mgrit_b200.so"
-SOURCES = ["rm_kernels.cu", "rm_big.cu", "rm_capi.cu"]
+SOURCES = ["rm_kernels.cu", "rm_big.cu", "rm_fft.cu", "rm_capi.cu"]
 HEADERS = ["rm_device.cuh", "rm_kernels.h"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

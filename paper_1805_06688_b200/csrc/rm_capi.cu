@@ -66,6 +66,13 @@ struct rm_grid {
   double lp_dmin = 0.0, lp_kmin = 0.0;  // min over the grid of the tau diagonals dm, dk
   double gen_absmax = 0.0;               // max |entry| of the six generator tables
   int max_clusters[5] = {0, 0, 0, 0, 0};
+  // FFT kernel (rm_fft.cu): 255^2 grids
+  bool fft_ok = false;
+  int fft_slots = 0;
+  double2* d_fsym = nullptr;
+  double* d_fscratch = nullptr;
+  double* d_dmT = nullptr;
+  double* d_dkT = nullptr;
 };
 
 extern "C" {
@@ -135,6 +142,11 @@ int rm_grid_create(int nx, int ny, const double* t1x_col, const double* t1x_row,
     tab[4 * GL + np - ny] = fy * t2y_col[ny - 1];
   }
   if (const char* m = getenv("RM_MERGE")) g->merge &= atoi(m);
+  std::vector<double> fsym;
+  if (rm::fft_supported(np, nx, ny)) {
+    fsym.resize(2 * 6 * 512);
+    rm::fft_symbols(tab.data(), np, GL, fsym.data());
+  }
   cudaError_t e;
   int maxc = 1;
   size_t scratch_per_cluster = 3 * (size_t)np * np;
@@ -180,6 +192,25 @@ int rm_grid_create(int nx, int ny, const double* t1x_col, const double* t1x_row,
     rm_grid_destroy(g);
     return cuda_fail(e, "rm_grid_create");
   }
+  if (!fsym.empty()) {
+    int nch = 0;
+    e = rm::fft_max_chains(&nch);
+    if (e != cudaSuccess || nch <= 0) {
+      cudaGetLastError();
+    } else {
+      nch = std::min(nch, g->big_slots);  // group barrier / reduction slots are shared with the DMMA kernel
+      if ((e = cudaMalloc(&g->d_fsym, sizeof(double) * fsym.size())) != cudaSuccess ||
+          (e = cudaMemcpy(g->d_fsym, fsym.data(), sizeof(double) * fsym.size(), cudaMemcpyHostToDevice)) !=
+              cudaSuccess ||
+          (e = cudaMalloc(&g->d_fscratch, sizeof(double) * rm::fft_scratch_doubles_per_chain() * nch)) !=
+              cudaSuccess) {
+        rm_grid_destroy(g);
+        return cuda_fail(e, "rm_grid_create (FFT kernel)");
+      }
+      g->fft_slots = nch;
+      g->fft_ok = true;
+    }
+  }
   *out = g;
   return RM_OK;
 }
@@ -198,6 +229,10 @@ int rm_grid_destroy(rm_grid* g) {
   cudaFree(g->d_dk);
   cudaFree(g->d_tab);
   cudaFree(g->d_dst16);
+  cudaFree(g->d_fsym);
+  cudaFree(g->d_fscratch);
+  cudaFree(g->d_dmT);
+  cudaFree(g->d_dkT);
   delete g;
   return RM_OK;
 }
@@ -271,10 +306,13 @@ int rm_sweep_run(rm_grid* g, const rm_sweep* sw, void* stream) {
   if (sw->out_div < 1) return fail(RM_EINVAL, "rm_sweep_run: out_div must be >= 1");
   if ((sw->explicit_rhs || sw->x0_mode == 1) && !sw->d_src) return fail(RM_EINVAL, "rm_sweep_run: d_src required");
   if (sw->x0_mode < 0 || sw->x0_mode > 4) return fail(RM_EINVAL, "rm_sweep_run: x0_mode must be 0..4");
-  if (sw->x0_mode == 4 && (sw->precond != 2 || !sw->lp_matvec || rm::big_supported(g->np) || g->nx != g->ny))
-    return fail(RM_EUNSUP, "rm_sweep_run: x0_mode 4 (split-FP16 apply probe) needs precond 2 with lp_matvec");
-  if (sw->x0_mode == 3 && (!sw->precond || rm::big_supported(g->np)))
-    return fail(RM_EUNSUP, "rm_sweep_run: x0_mode 3 (preconditioner probe) needs precond > 0 and a grid up to 127^2");
+  const bool use_fft = g->fft_ok && !(getenv("RM_NO_FFT") && atoi(getenv("RM_NO_FFT")));
+  if (sw->x0_mode == 4 && !use_fft &&
+      (sw->precond != 2 || !sw->lp_matvec || rm::big_supported(g->np) || g->nx != g->ny))
+    return fail(RM_EUNSUP, "rm_sweep_run: x0_mode 4 (apply probe) needs the FFT kernel or precond 2 with lp_matvec");
+  if (sw->x0_mode == 3 && (!sw->precond || (rm::big_supported(g->np) && !use_fft)))
+    return fail(RM_EUNSUP, "rm_sweep_run: x0_mode 3 (preconditioner probe) needs precond > 0 and a grid up to 127^2 "
+                           "or the FFT kernel");
   if (sw->x0_mode == 2 && !sw->d_x0) return fail(RM_EINVAL, "rm_sweep_run: d_x0 required for x0_mode 2");
   if (sw->clen > 1 && (!sw->d_out || sw->out_div != 1))
     return fail(RM_EINVAL, "rm_sweep_run: chains longer than one step need d_out with out_div == 1");
@@ -282,6 +320,37 @@ int rm_sweep_run(rm_grid* g, const rm_sweep* sw, void* stream) {
   if (!(sw->rel_tol > 0)) return fail(RM_EINVAL, "relative tolerance must be positive");
   if (sw->precond < 0 || sw->precond > 2) return fail(RM_EINVAL, "rm_sweep_run: precond must be 0, 1 or 2");
   if (sw->precond && !g->d_dm) return fail(RM_EINVAL, "rm_sweep_run: precond needs rm_grid_set_tau first");
+  if (use_fft) {
+    if (sw->group > 0 && sw->group != rm::fft_group())
+      return fail(RM_EUNSUP, "rm_sweep_run: the FFT kernel uses a fixed group size");
+    if (sw->precond && !g->d_dmT) return fail(RM_EINVAL, "rm_sweep_run: precond needs rm_grid_set_tau first");
+    rm::ChainArgs a = {};
+    a.gbar = g->d_gbar;
+    a.gbuf = g->d_gbuf;
+    a.sw = *sw;
+    a.sw.lp_matvec = 0;
+    if (a.sw.precond) a.sw.precond = 1;  // FP64 throughout (the DST stages are FFTs)
+    a.nx = g->nx;
+    a.ny = g->ny;
+    a.cm = g->cm;
+    a.gens = g->d_gens;
+    a.merge = g->merge;
+    a.chain_counter = g->d_counter;
+    a.fail = g->d_fail;
+    a.fail_info = g->d_fail_info;
+    a.timing = g->d_timing;
+    a.dm = g->d_dm;
+    a.dk = g->d_dk;
+    a.fsym = g->d_fsym;
+    a.fscratch = g->d_fscratch;
+    a.dmT = g->d_dmT;
+    a.dkT = g->d_dkT;
+    cudaStream_t stf = (cudaStream_t)stream;
+    RM_CUDA(cudaMemsetAsync(g->d_counter, 0, sizeof(int), stf), "rm_sweep_run: counter reset");
+    RM_CUDA(cudaMemsetAsync(g->d_gbar, 0, sizeof(unsigned) * 32 * g->fft_slots, stf), "rm_sweep_run: barriers");
+    RM_CUDA(rm::launch_fft(a, g->fft_slots, stf), "rm_sweep_run: launch (FFT kernel)");
+    return RM_OK;
+  }
   if (rm::big_supported(g->np)) {
     if (sw->group > 0 && sw->group != rm::big_group(g->np))
       return fail(RM_EUNSUP, "rm_sweep_run: the large-grid kernel uses a fixed cluster size");
@@ -378,6 +447,19 @@ int rm_grid_set_tau(rm_grid* g, const double* dm, const double* dk) {
   RM_CUDA(cudaMemcpy(g->d_dm, dm, n * sizeof(double), cudaMemcpyHostToDevice), "rm_grid_set_tau");
   RM_CUDA(cudaMemcpy(g->d_dk, dk, n * sizeof(double), cudaMemcpyHostToDevice), "rm_grid_set_tau");
   RM_CUDA(cudaMemcpy(g->d_tab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice), "rm_grid_set_tau");
+  if (g->fft_ok) {
+    std::vector<double> mt(n), kt(n);
+    for (int a = 0; a < g->ny; ++a)
+      for (int b = 0; b < g->nx; ++b) {
+        mt[(size_t)b * g->ny + a] = dm[(size_t)a * g->nx + b];
+        kt[(size_t)b * g->ny + a] = dk[(size_t)a * g->nx + b];
+      }
+    if (!g->d_dmT && ((e = cudaMalloc(&g->d_dmT, n * sizeof(double))) != cudaSuccess ||
+                      (e = cudaMalloc(&g->d_dkT, n * sizeof(double))) != cudaSuccess))
+      return cuda_fail(e, "rm_grid_set_tau");
+    RM_CUDA(cudaMemcpy(g->d_dmT, mt.data(), n * sizeof(double), cudaMemcpyHostToDevice), "rm_grid_set_tau");
+    RM_CUDA(cudaMemcpy(g->d_dkT, kt.data(), n * sizeof(double), cudaMemcpyHostToDevice), "rm_grid_set_tau");
+  }
   g->lp_dmin = dm[0];
   g->lp_kmin = dk[0];
   for (size_t i = 1; i < n; ++i) {

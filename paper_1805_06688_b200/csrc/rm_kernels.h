@@ -29,6 +29,11 @@ struct ChainArgs {
   const uint16_t* dst16; // FP16 DST-I matrix [NP][NP+8] of the low-precision tau stages (precond 2, nx == ny)
   double lp_dmin, lp_kmin; // min over the grid of dm, dk: 1/(lp_dmin + s lp_kmin) bounds max 1/d(s)
   double gen_absmax;       // max |entry| of the six generator tables (split-FP16 table scaling)
+  // FFT kernel (rm_fft.cu, 255^2 grids)
+  const double2* fsym;     // 6 stiffness spectra (512 points each), k-layout order
+  double* fscratch;        // per-chain vectors (fft_scratch_doubles_per_chain each)
+  const double* dmT;       // tau diagonals transposed, [nx][ny]
+  const double* dkT;
 };
 
 struct ApplyArgs {
@@ -64,6 +69,12 @@ size_t big_scratch_doubles_per_cluster(int np);
 cudaError_t launch_big(int np, const ChainArgs& a, int max_clusters, cudaStream_t st);
 cudaError_t big_max_clusters(int np, int* out);
 cudaError_t launch_apply_big(int np, const ApplyArgs& a, int batch, cudaStream_t st);
+bool fft_supported(int np, int nx, int ny);
+int fft_group();
+size_t fft_scratch_doubles_per_chain();
+cudaError_t fft_max_chains(int* out);
+cudaError_t launch_fft(const ChainArgs& a, int max_chains, cudaStream_t st);
+void fft_symbols(const double* tab, int np, int gl, double* out_klayout);
 cudaError_t launch_diff_sqnorm(int64_t n, const double* a, const double* b, double* out, cudaStream_t st);
 
 }  // namespace rm

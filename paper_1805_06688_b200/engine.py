@@ -261,6 +261,18 @@ class Engine:
                    explicit=False, x0_mode=4, f=(V, -1), f_stride=self.ndof, out=(out, -1), precond="tau")
         return out
 
+    def apply_probe(self, V: torch.Tensor, dt: torch.Tensor) -> torch.Tensor:
+        """(M + dt[b]/2 K) V[b] through the chain kernel's own FP64 operator (rm_sweep x0_mode 4; the FFT
+        kernel's grids; probe for tests)."""
+        V = V.reshape(-1, self.ndof).contiguous()
+        B = V.shape[0]
+        out = torch.empty_like(V)
+        cnt = torch.zeros(5, dtype=torch.int64, device=V.device)
+        dt = dt.reshape(-1).to(torch.float64).contiguous()
+        self.sweep(nchains=B, first=1, cstride=1, clen=1, nmax=B, dt=dt, counters=cnt, rel_tol=1.0,
+                   explicit=False, x0_mode=4, f=(V, -1), f_stride=self.ndof, out=(out, -1), precond="none")
+        return out
+
     def check_fail(self) -> None:
         """Raise CgFailure for the first failed solve since the last reset (synchronises)."""
         code, n, its, res = C.c_int(), C.c_int(), C.c_int64(), C.c_double()

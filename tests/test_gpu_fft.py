@@ -1,0 +1,74 @@
+"""The FFT chain kernel (csrc/rm_fft.cu; 255^2 grids, BASELINE config 3) against the CPU oracle.
+
+Its operator is evaluated through 512-point FFTs (circulant embedding of the Toeplitz blocks) and its tau
+preconditioner's DST-I through odd-extended FFTs, all in FP64: the probes below pin both against the
+oracle's dense operator (reference assembly.py:100-115, 155-161) and the numpy DST preconditioner
+(precond.py), and propagations against the oracle's CG (krylov.py:32-92).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import riesz_oracle as O
+from paper_1805_06688_b200.configs import make_case
+from paper_1805_06688_b200.engine import Engine
+from paper_1805_06688_b200.precond import dst_matrix, tau_diagonals
+from paper_1805_06688_b200.krylov import CgOptions
+from paper_1805_06688_b200.stepper import Discretization, ProblemSpec
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300)
+
+
+def vectors(g, rng):
+    x, y = np.meshgrid(np.arange(1, g.nx + 1) / (g.nx + 1), np.arange(1, g.ny + 1) / (g.ny + 1))
+    return np.stack([rng.standard_normal(g.ndof), (np.sin(np.pi * x) * np.sin(np.pi * y)).ravel(),
+                     rng.random(g.ndof), ((-1.0) ** np.arange(g.ndof)) * 3e5])
+
+
+@pytest.mark.parametrize("name", ["cfg3"])
+def test_fft_apply_matches_oracle(name):
+    case = make_case(name, Nt=8)
+    g = case.grid
+    eng = Engine.for_problem(g, case.beta, case.gamma, case.kx, case.ky)
+    ops = O.Operators(O.Grid(g.mx, g.my), case.kx, case.ky, case.beta, case.gamma)
+    V = vectors(g, np.random.default_rng(3))
+    dts = np.array([1.0 / 16384, 1.0 / 64, 0.5, 1.0 / 1024])
+    got = eng.apply_probe(torch.from_numpy(V).cuda(), torch.from_numpy(dts).cuda()).cpu().numpy()
+    for k in range(4):
+        ref = ops.step_apply(dts[k], +1, V[k])
+        assert rel(got[k], ref) <= 1e-13, (k, rel(got[k], ref))
+
+
+def test_fft_precond_matches_numpy():
+    case = make_case("cfg3", Nt=8)
+    g = case.grid
+    eng = Engine.for_problem(g, case.beta, case.gamma, case.kx, case.ky)
+    dm, dk = tau_diagonals(g, case.beta, case.gamma, case.kx, case.ky)
+    Sx, Sy = dst_matrix(g.nx), dst_matrix(g.ny)
+    V = vectors(g, np.random.default_rng(4))[:3]
+    dts = np.array([1.0 / 16384, 0.25, 1.0 / 64])
+    ref = np.stack([(Sy @ ((Sy @ v.reshape(g.ny, g.nx) @ Sx) / (dm + 0.5 * dt * dk)) @ Sx).ravel()
+                    for v, dt in zip(V, dts)])
+    got = eng.precond_apply(torch.from_numpy(V).cuda(), torch.from_numpy(dts).cuda(), "tau64").cpu().numpy()
+    for k in range(3):
+        assert rel(got[k], ref[k]) <= 1e-12, (k, rel(got[k], ref[k]))
+
+
+@pytest.mark.parametrize("pre", ["none", "tau"])
+def test_fft_propagate_matches_oracle(pre):
+    case = make_case("cfg3", Nt=4)
+    g = case.grid
+    spec = ProblemSpec(**case.problem_kwargs())
+    disc = Discretization(spec, cg_opts=CgOptions(rel_tol=1e-12, preconditioner=pre))
+    st = O.Stepper(O.Problem(O.Grid(g.mx, g.my), spec.tmesh.points, case.kx, case.ky, case.beta, case.gamma,
+                             spec.source, spec.initial), rel_tol=1e-12)
+    V = np.random.default_rng(1).random((3, g.ndof))
+    for dt in (1.0 / 16384, 1.0 / 1024, 1.0 / 16):
+        got = disc.propagate(dt, V)
+        for k in range(3):
+            assert rel(got[k], st.propagate(dt, V[k])) <= 1e-10
