@@ -45,11 +45,14 @@ constexpr int RS = NP / G;            // rows (columns) per CTA
 constexpr int H = RS / 2;             // packing partner offset
 constexpr int THREADS = 512;
 constexpr int WARPS = 16;
+constexpr int NOWN = 2;               // owner rows per thread (one packed pair per warp)
+constexpr int PPW = NOWN / 2;          // packed pairs per warp
 constexpr int NSLOT = H + 2;          // packed pairs incl. the +-1 halo
 constexpr int SLOT = 548;             // double2 per slot: >= 16 x 34 transpose scratch
 constexpr int TS = 34;                // transpose row stride (conflict-free 16-byte accesses)
 constexpr int NVEC = 6;               // per-chain vectors
 constexpr size_t VEC = (size_t)NP * NP;
+constexpr size_t DIV = (size_t)H * 16 * 32 * 2;  // per-CTA 1/d(s) cache (doubles)
 constexpr size_t SMEM = sizeof(double2) * ((size_t)NSLOT * SLOT + L + 16 + 6 * L) + sizeof(double) * (4 * 32) + 64;
 static_assert(SMEM <= 227 * 1024, "shared memory budget");
 
@@ -272,273 +275,392 @@ __device__ __forceinline__ void greduce(double (&part)[NV], double* wred, Sync& 
   buf ^= 1;
 }
 
-}  // namespace fft
 
-#define RM_OWN_FOR _Pragma("unroll") for (int p = 0; p < 2; ++p) _Pragma("unroll") for (int m = 0; m < 8; ++m)
-
-template <bool PRE>
-__global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const ChainArgs P) {
-  using namespace fft;
-  extern __shared__ __align__(16) double2 sm2[];
-  double2* slots = sm2;                  // NSLOT x SLOT
-  double2* tw2 = slots + NSLOT * SLOT;   // tw2[q * 32 + t] = W512^{q t}
-  double2* tw32 = tw2 + L;               // W32^r = W512^{16 r}
-  double2* sym = tw32 + 16;              // 6 stiffness spectra in k-layout
-  double* wred = reinterpret_cast<double*>(sym + 6 * L);
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int rank = blockIdx.x % G;
-  const int R0 = RS * rank, C0 = RS * rank;
-  const int cid = blockIdx.x / G;
-
+// ---- per-CTA context and the kernel's building blocks (all force-inlined: the owner vectors stay in
+// registers across them) ------------------------------------------------------------------------------
+struct Ctx {
+  double* base;        // this chain's vectors
+  const ChainArgs* P;
+  int rank;
+  double di_s;         // s of the cached DI (NaN: none)
   Sync sy;
-  sy.gbar = P.gbar + (size_t)cid * 32;
-  sy.gred = P.gbuf + (size_t)cid * 1024;
-  sy.sched = reinterpret_cast<int*>(sy.gred + 8 * G);
-  sy.epoch = 0;
-
-  for (int i = tid; i < L; i += THREADS) {
-    const int q = i >> 5, t = i & 31;
-    double sn, cs;
-    sincospi(-2.0 * (double)(q * t) / (double)L, &sn, &cs);
-    tw2[i] = make_double2(cs, sn);
+  int buf;
+  __device__ __forceinline__ int tid() const { return threadIdx.x; }
+  __device__ __forceinline__ int lane() const { return threadIdx.x & 31; }
+  __device__ __forceinline__ int warp() const { return threadIdx.x >> 5; }
+  __device__ __forceinline__ int R0() const { return RS * rank; }
+  __device__ __forceinline__ int C0() const { return RS * rank; }
+  __device__ __forceinline__ double* PV() const { return base; }            // operand (read across CTAs)
+  __device__ __forceinline__ double* WV() const { return base + VEC; }      // y-pass output
+  __device__ __forceinline__ double* SR() const { return base + 2 * VEC; }  // row-DST output
+  __device__ __forceinline__ double* XV() const { return base + 3 * VEC; }  // iterate (owner rows)
+  __device__ __forceinline__ double* RV() const { return base + 4 * VEC; }  // residual
+  __device__ __forceinline__ double* BV() const { return base + 5 * VEC; }  // right-hand side
+  // this CTA's 1/d(s) of its column pairs, k-layout [warp][r][lane]
+  __device__ __forceinline__ double2* DI() const {
+    return reinterpret_cast<double2*>(base + NVEC * VEC + (size_t)rank * DIV);
   }
-  if (tid < 16) {
-    double sn, cs;
-    sincospi(-2.0 * (double)(16 * tid) / (double)L, &sn, &cs);
-    tw32[tid] = make_double2(cs, sn);
+};
+
+__device__ __forceinline__ double2* smem2() {
+  extern __shared__ __align__(16) double2 fft_smem[];
+  return fft_smem;
+}
+__device__ __forceinline__ double2* SLOTS() { return smem2(); }
+__device__ __forceinline__ const double2* TW2() { return smem2() + NSLOT * SLOT; }
+__device__ __forceinline__ const double2* TW32() { return smem2() + NSLOT * SLOT + L; }
+__device__ __forceinline__ const double2* SYM() { return smem2() + NSLOT * SLOT + L + 16; }
+__device__ __forceinline__ double* WRED() { return reinterpret_cast<double*>(smem2() + NSLOT * SLOT + L + 16 + 6 * L); }
+constexpr int NX = NP - 1;  // the kernel serves n = 255 grids only (fft_supported)
+constexpr double HALF_C = 0.044194173824159220;  // sqrt(2 / 256) / 2
+
+#define RM_OWN_FOR _Pragma("unroll") for (int p = 0; p < NOWN; ++p) _Pragma("unroll") for (int m = 0; m < 8; ++m)
+
+// owner rows of thread (warp w, lane t): pairs q = w + WARPS (p >> 1), component p & 1 -> row R0 + q + H (p & 1)
+__device__ __forceinline__ int own_j(const Ctx& c, int p) { return c.R0() + c.warp() + WARPS * (p >> 1) + H * (p & 1); }
+__device__ __forceinline__ int own_i(const Ctx& c, int m) { return c.lane() + 32 * m; }
+__device__ __forceinline__ int own_e(const Ctx& c, int p, int m) { return own_j(c, p) * NP + own_i(c, m); }
+__device__ __forceinline__ bool own_valid(const Ctx& c, int p, int m) { return own_j(c, p) < NX && own_i(c, m) < NX; }
+
+template <int NV>
+__device__ __forceinline__ void creduce(Ctx& c, double (&part)[NV], double (&out)[NV]) {
+  greduce<NV>(part, WRED(), c.sy, c.buf, c.rank, c.warp(), c.lane(), out);
+}
+
+// M v of the owner rows from PV (7-point P1 mass; per step, not per iteration)
+__device__ __forceinline__ void mass_own(const Ctx& c, double (&out)[NOWN][8]) {
+  RM_OWN_FOR {
+    const int j = own_j(c, p), i = own_i(c, m);
+    const double* q = c.PV() + j * NP + i;
+    double s = 0.0;
+    if (own_valid(c, p, m)) {
+      const double up = __ldcg(q + NP), upr = __ldcg(q + NP + 1), ce = __ldcg(q), r = __ldcg(q + 1);
+      const double l = i > 0 ? __ldcg(q - 1) : 0.0;
+      const double dn = j > 0 ? __ldcg(q - NP) : 0.0;
+      const double dnl = (j > 0 && i > 0) ? __ldcg(q - NP - 1) : 0.0;
+      s = c.P->cm * (6.0 * ce + l + r + up + upr + dn + dnl);
+    }
+    out[p][m] = s;
   }
-  for (int i = tid; i < 6 * L; i += THREADS) sym[i] = P.fsym[i];
+}
 
-  const rm_sweep& W_ = P.sw;
-  const int nx = P.nx, ny = P.ny;
-  const double cm = P.cm;
-  const int64_t max_iter = W_.max_iter > 0 ? W_.max_iter : 10 * (int64_t)nx * ny;
-  const bool need_in = W_.explicit_rhs || W_.x0_mode == 1;
-  const double half_c = 0.5 * sqrt(2.0 / (double)(nx + 1));
-  const double inv_l = 1.0 / (double)L;
-
-  double* base = P.fscratch + (size_t)cid * NVEC * VEC;
-  double* PV = base;            // operand (read across CTAs)
-  double* WV = base + VEC;      // y-pass output
-  double* SR = base + 2 * VEC;  // row-DST output
-  double* XV = base + 3 * VEC;  // iterate (owner rows)
-  double* RV = base + 4 * VEC;  // residual
-  double* BV = base + 5 * VEC;  // right-hand side
-  // zero this chain slot's vectors once (padding row / column 255 is never written afterwards)
-  for (size_t i = (size_t)rank * THREADS + tid; i < NVEC * VEC; i += (size_t)G * THREADS) base[i] = 0.0;
-  int buf = 0;
-  gsync(sy);
-
-  auto own_j = [&](int p) { return R0 + warp + H * p; };
-  auto own_i = [&](int m) { return lane + 32 * m; };
-  auto valid = [&](int j, int i) { return j < ny && i < nx; };
-  auto pv = [&](int j, int i) -> double { return (j >= 0 && i >= 0) ? __ldcg(PV + j * NP + i) : 0.0; };
-  auto mass_pv = [&](int j, int i) -> double {
-    double s = 6.0 * pv(j, i);
-    s += pv(j, i - 1);
-    s += pv(j, i + 1);
-    s += pv(j + 1, i);
-    s += pv(j + 1, i + 1);
-    s += pv(j - 1, i);
-    s += pv(j - 1, i - 1);
-    return cm * s;
-  };
-
-  // ---- y-direction pass of the stiffness apply: WV[:, own columns] = (1/L) sum_t IFFT(S_t FFT(PV col +- 0/1))
-  auto col_pass_apply = [&]() {
-    // stage columns C0-1 .. C0+32 into slots s = 0..17 (pair (C0+s-1, C0+s+15)), natural row order
-    for (int idx = tid; idx < NP * 34; idx += THREADS) {
-      const int j = idx / 34, o = idx % 34 - 1, c = C0 + o;
-      const double v = (c >= 0 && c < NP) ? __ldcg(PV + j * NP + c) : 0.0;
-      if (o <= 16) slots[(o + 1) * SLOT + j].x = v;
-      if (o >= 15) slots[(o - 15) * SLOT + j].y = v;
-    }
-    for (int idx = tid; idx < NSLOT * (L - NP); idx += THREADS)
-      slots[(idx / (L - NP)) * SLOT + NP + idx % (L - NP)] = make_double2(0.0, 0.0);
-    __syncthreads();
-    for (int s = warp; s < NSLOT; s += WARPS) {
-      double2 a[16];
-      double2* sl = slots + s * SLOT;
+// y-direction pass of the stiffness: WV[:, own columns] = (1/L) sum_t IFFT(S_t FFT(PV columns i + 0/+1/-1))
+__device__ __forceinline__ void col_pass_apply(Ctx& c) {
+  double2* slots = SLOTS();
+  // stage columns C0-1 .. C0+32 into slots s = 0..17 (pair (C0+s-1, C0+s+15)), natural row order; a warp
+  // covers 34 consecutive columns of one row per step (coalesced)
+  for (int j = c.warp(); j < NP; j += WARPS) {
+    const double* row = c.PV() + j * NP + c.C0();
 #pragma unroll
-      for (int m = 0; m < 16; ++m) a[m] = sl[lane + 32 * m];
-      fft512_fwd(a, sl, tw2, tw32, lane);
-      __syncwarp();
-#pragma unroll
-      for (int r = 0; r < 16; ++r) sl[r * 32 + lane] = a[r];
-    }
-    __syncthreads();
-    double2 a[16];
-    {
-      const double2* s0 = slots + (warp + 1) * SLOT;  // columns i
-      const double2* sp = s0 + SLOT;                  // columns i + 1
-      const double2* sm = s0 - SLOT;                  // columns i - 1
-#pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        const int e = r * 32 + lane;
-        double2 y = cmul(sym[3 * L + e], s0[e]);
-        y = cadd(y, cmul(sym[4 * L + e], sp[e]));
-        a[r] = cadd(y, cmul(sym[5 * L + e], sm[e]));
+    for (int h = 0; h < 2; ++h) {  // the strip's 34 columns: two passes of the warp
+      const int o = c.lane() + 32 * h - 1;
+      if (o <= 32) {
+        const int col = c.C0() + o;
+        const double v = (col >= 0 && col < NP) ? __ldcg(row + o) : 0.0;
+        if (o <= 16) slots[(o + 1) * SLOT + j].x = v;
+        if (o >= 15) slots[(o - 15) * SLOT + j].y = v;
       }
     }
-    __syncthreads();
-    {
-      double2* sl = slots + (warp + 1) * SLOT;
-      fft512_inv(a, sl, tw2, tw32, lane);
-      __syncwarp();
-#pragma unroll
-      for (int m = 0; m < 8; ++m) sl[lane + 32 * m] = cscale(a[m], inv_l);
-    }
-    __syncthreads();
-    for (int idx = tid; idx < NP * RS; idx += THREADS) {
-      const int j = idx / RS, o = idx % RS;
-      const double2 t = slots[(o < H ? o + 1 : o - H + 1) * SLOT + j];
-      WV[j * NP + C0 + o] = o < H ? t.x : t.y;
-    }
-  };
-
-  // ---- x-direction pass for the owner rows: acc = (1/L) sum_t IFFT(S_t FFT(PV rows j + 0/+1/-1))
-  auto row_pass_apply = [&](double (&acc)[2][8]) {
-    for (int s = warp; s < NSLOT; s += WARPS) {
-      const int ja = R0 + s - 1, jb = R0 + s - 1 + H;
-      double2 a[16];
-#pragma unroll
-      for (int m = 0; m < 16; ++m) {
-        const int i = lane + 32 * m;
-        a[m] = make_double2(m < 8 && ja >= 0 && ja < NP ? __ldcg(PV + ja * NP + i) : 0.0,
-                            m < 8 && jb < NP ? __ldcg(PV + jb * NP + i) : 0.0);
-      }
-      double2* sl = slots + s * SLOT;
-      fft512_fwd(a, sl, tw2, tw32, lane);
-      __syncwarp();
-#pragma unroll
-      for (int r = 0; r < 16; ++r) sl[r * 32 + lane] = a[r];
-    }
-    __syncthreads();
+  }
+  for (int idx = c.tid(); idx < NSLOT * (L - NP); idx += THREADS)
+    slots[(idx / (L - NP)) * SLOT + NP + idx % (L - NP)] = make_double2(0.0, 0.0);
+  __syncthreads();
+  for (int s = c.warp(); s < NSLOT; s += WARPS) {
     double2 a[16];
-    {
-      const double2* s0 = slots + (warp + 1) * SLOT;
+    double2* sl = slots + s * SLOT;
+#pragma unroll
+    for (int m = 0; m < 16; ++m) a[m] = sl[c.lane() + 32 * m];
+    fft512_fwd(a, sl, TW2(), TW32(), c.lane());
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < 16; ++r) sl[r * 32 + c.lane()] = a[r];
+  }
+  __syncthreads();
+  double2 a[PPW][16];  // output pairs q = warp + WARPS h
+#pragma unroll
+  for (int h = 0; h < PPW; ++h) {
+    const double2* s0 = slots + (c.warp() + WARPS * h + 1) * SLOT;  // columns i
+    const double2* sp = s0 + SLOT;                              // columns i + 1
+    const double2* sm = s0 - SLOT;                              // columns i - 1
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const int e = r * 32 + c.lane();
+      double2 y = cmul(SYM()[3 * L + e], s0[e]);
+      y = cadd(y, cmul(SYM()[4 * L + e], sp[e]));
+      a[h][r] = cadd(y, cmul(SYM()[5 * L + e], sm[e]));
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int h = 0; h < PPW; ++h) {
+    double2* sl = slots + (c.warp() + WARPS * h + 1) * SLOT;
+    fft512_inv(a[h], sl, TW2(), TW32(), c.lane());
+    __syncwarp();
+    constexpr double inv_l = 1.0 / (double)L;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) sl[c.lane() + 32 * m] = cscale(a[h][m], inv_l);
+  }
+  __syncthreads();
+  // store the 32 own columns, one row per warp step
+  for (int j = c.warp(); j < NP; j += WARPS) {
+    const int o = c.lane();
+    const double2 t = slots[(o < H ? o + 1 : o - H + 1) * SLOT + j];
+    c.WV()[j * NP + c.C0() + o] = o < H ? t.x : t.y;
+  }
+}
+
+// x-direction pass for the owner rows with the P1 mass folded in: acc = (1/L) sum_t IFFT((sg S_t + cm M_t) FFT(PV
+// rows j + 0/+1/-1)); the mass blocks tridiag(1,6,1), (1 at d = 0,-1), (1 at d = 0,+1) have the spectra
+// 6 + 2 cos(theta), 1 + e^{i theta}, 1 + e^{-i theta}, theta = 2 pi k / L (rm_device.cuh build_step_tables)
+__device__ __forceinline__ void row_pass_apply(Ctx& c, double (&acc)[NOWN][8], double sg) {
+  double2* slots = SLOTS();
+  for (int s = c.warp(); s < NSLOT; s += WARPS) {
+    const int ja = c.R0() + s - 1, jb = c.R0() + s - 1 + H;
+    double2 a[16];
+    const double* ra = c.PV() + ja * NP + c.lane();
+    const double* rb = c.PV() + jb * NP + c.lane();
+    const bool va = ja >= 0, vb = jb < NP;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) a[m] = make_double2(va ? __ldcg(ra + 32 * m) : 0.0, vb ? __ldcg(rb + 32 * m) : 0.0);
+#pragma unroll
+    for (int m = 8; m < 16; ++m) a[m] = make_double2(0.0, 0.0);
+    double2* sl = slots + s * SLOT;
+    fft512_fwd(a, sl, TW2(), TW32(), c.lane());
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < 16; ++r) sl[r * 32 + c.lane()] = a[r];
+  }
+  __syncthreads();
+  double2 a[PPW][16];  // output pairs q = warp + WARPS h
+  {
+    const double2 w0 = TW2()[32 + (c.lane() >> 1)];  // W512^{q}
+    const double sgn = (c.lane() & 1) ? -1.0 : 1.0;   // W512^{256 v}
+    const double cm = c.P->cm;
+#pragma unroll
+    for (int h = 0; h < PPW; ++h) {
+      const double2* s0 = slots + (c.warp() + WARPS * h + 1) * SLOT;
       const double2* sp = s0 + SLOT;
       const double2* sm = s0 - SLOT;
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
-        const int e = r * 32 + lane;
-        double2 y = cmul(sym[0 * L + e], s0[e]);
-        y = cadd(y, cmul(sym[1 * L + e], sp[e]));
-        a[r] = cadd(y, cmul(sym[2 * L + e], sm[e]));
+        const int e = r * 32 + c.lane();
+        const double2 w = cscale(cmul(w0, TW32()[r]), sgn);  // e^{-i theta_k}
+        const double2 s0v = SYM()[e], s1v = SYM()[L + e], s2v = SYM()[2 * L + e];
+        const double2 c0 = make_double2(fma(sg, s0v.x, cm * (6.0 + 2.0 * w.x)), sg * s0v.y);
+        const double2 c1 = make_double2(fma(sg, s1v.x, cm * (1.0 + w.x)), fma(sg, s1v.y, -cm * w.y));
+        const double2 c2 = make_double2(fma(sg, s2v.x, cm * (1.0 + w.x)), fma(sg, s2v.y, cm * w.y));
+        double2 y = cmul(c0, s0[e]);
+        y = cadd(y, cmul(c1, sp[e]));
+        a[h][r] = cadd(y, cmul(c2, sm[e]));
       }
     }
-    __syncthreads();
-    fft512_inv(a, slots + (warp + 1) * SLOT, tw2, tw32, lane);
+  }
+  __syncthreads();
+  constexpr double inv_l = 1.0 / (double)L;
+#pragma unroll
+  for (int h = 0; h < PPW; ++h) {
+    fft512_inv(a[h], slots + (c.warp() + WARPS * h + 1) * SLOT, TW2(), TW32(), c.lane());
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
-      acc[0][m] = a[m].x * inv_l;
-      acc[1][m] = a[m].y * inv_l;
+      acc[2 * h][m] = a[h][m].x * inv_l;
+      acc[2 * h + 1][m] = a[h][m].y * inv_l;
     }
-  };
+  }
+}
 
-  // acc = (M + sg K) PV for the owner rows (PV complete and visible; one group barrier inside)
-  auto apply_pv = [&](double (&acc)[2][8], double sg) {
-    col_pass_apply();
-    gsync(sy);
-    row_pass_apply(acc);
-    RM_OWN_FOR {
-      const int j = own_j(p), i = own_i(m);
-      acc[p][m] = valid(j, i) ? mass_pv(j, i) + sg * (acc[p][m] + __ldcg(WV + j * NP + i)) : 0.0;
-    }
-  };
+// acc = (M + sg K) PV for the owner rows (PV complete and visible; one group barrier inside)
+__device__ __forceinline__ void apply_pv(Ctx& c, double (&acc)[NOWN][8], double sg) {
+  col_pass_apply(c);
+  gsync(c.sy);
+  row_pass_apply(c, acc, sg);
+  double wv[NOWN][8];
+  RM_OWN_FOR { wv[p][m] = __ldcg(c.WV() + own_e(c, p, m)); }
+  RM_OWN_FOR { acc[p][m] = own_valid(c, p, m) ? fma(sg, wv[p][m], acc[p][m]) : 0.0; }
+}
 
-  // z = P(s)^-1 r = (Sy x Sx) diag(1/d(s)) (Sy x Sx) r for the owner rows (two group barriers)
-  auto precond = [&](const double (&r)[2][8], double (&z)[2][8], double s) {
-    {  // SR[own rows] = Sx r (x-frequency along the row)
-      double2 a[16];
-#pragma unroll
-      for (int m = 0; m < 8; ++m) a[m] = make_double2(r[0][m], r[1][m]);
-      double2* sl = slots + warp * SLOT;
-      dst_fwd(a, sl, tw2, tw32, lane, half_c);
-      if ((lane & 1) == 0) {
-#pragma unroll
-        for (int rr = 0; rr < 16; ++rr) {
-          const int k = klay(lane, rr);
-          if (k >= 1 && k <= 255) {
-            SR[own_j(0) * NP + k - 1] = a[rr].x;
-            SR[own_j(1) * NP + k - 1] = a[rr].y;
-          }
-        }
+// refresh this CTA's 1/d(s) cache when s changed (once per sweep on uniform levels)
+__device__ __forceinline__ void dinv_refresh(Ctx& c, double s) {
+  if (s == c.di_s) return;
+  c.di_s = s;
+#pragma unroll 1
+  for (int h = 0; h < PPW; ++h) {
+    const int q = c.warp() + WARPS * h;
+    const int ca = c.C0() + q, cb = c.C0() + q + H;  // x-frequencies of the column pair
+#pragma unroll 4
+    for (int r = 0; r < 16; ++r) {
+      const int k = klay(c.lane(), r);
+      const int kk = k <= 256 ? k : 512 - k;
+      double2 w = make_double2(0.0, 0.0);
+      if (kk >= 1 && kk <= 255) {
+        const int a = kk - 1;
+        if (ca < NX) w.x = 1.0 / (__ldg(c.P->dmT + ca * NX + a) + s * __ldg(c.P->dkT + ca * NX + a));
+        if (cb < NX) w.y = 1.0 / (__ldg(c.P->dmT + cb * NX + a) + s * __ldg(c.P->dkT + cb * NX + a));
       }
+      c.DI()[(q * 16 + r) * 32 + c.lane()] = w;
     }
-    gsync(sy);
-    {  // column pass: WV[:, own columns] = Sy diag(1/d) Sy SR
-      for (int idx = tid; idx < NP * RS; idx += THREADS) {
-        const int j = idx / RS, o = idx % RS;
-        const double v = __ldcg(SR + j * NP + C0 + o);
-        if (o < H)
-          slots[(o + 1) * SLOT + j].x = v;
-        else
-          slots[(o - H + 1) * SLOT + j].y = v;
-      }
-      __syncthreads();
-      double2* sl = slots + (warp + 1) * SLOT;
-      double2 a[16];
+  }
+}
+
+// z = P(s)^-1 r = (Sy x Sx) diag(1/d(s)) (Sy x Sx) r for the owner rows (two group barriers)
+__device__ __forceinline__ void precond(Ctx& c, const double (&r)[NOWN][8], double (&z)[NOWN][8], double s) {
+  double2* slots = SLOTS();
+  dinv_refresh(c, s);
+#pragma unroll 1
+  for (int h = 0; h < PPW; ++h) {  // SR[own rows] = Sx r (x-frequency along the row), pairs q = warp + WARPS h
+    double2 a[16];
 #pragma unroll
-      for (int m = 0; m < 8; ++m) a[m] = sl[lane + 32 * m];
-      dst_fwd(a, sl, tw2, tw32, lane, half_c);
-      const int ca = C0 + warp, cb = C0 + warp + H;  // x-frequencies of the pair
+    for (int m = 0; m < 8; ++m) a[m] = make_double2(r[2 * h][m], r[2 * h + 1][m]);
+    dst_fwd(a, slots + (c.warp() + WARPS * h) * SLOT, TW2(), TW32(), c.lane(), HALF_C);
+    if ((c.lane() & 1) == 0) {
+      double* sa = c.SR() + own_j(c, 2 * h) * NP - 1;
+      double* sb = c.SR() + own_j(c, 2 * h + 1) * NP - 1;
 #pragma unroll
       for (int rr = 0; rr < 16; ++rr) {
-        const int k = klay(lane, rr);
-        const int kk = k <= 256 ? k : 512 - k;
-        double2 w = make_double2(0.0, 0.0);
-        if (kk >= 1 && kk <= 255) {
-          const double da = ca < nx ? __ldg(P.dmT + ca * nx + kk - 1) + s * __ldg(P.dkT + ca * nx + kk - 1) : 1.0;
-          const double db = cb < nx ? __ldg(P.dmT + cb * nx + kk - 1) + s * __ldg(P.dkT + cb * nx + kk - 1) : 1.0;
-          w = make_double2(a[rr].x * rcp_fast(da), a[rr].y * rcp_fast(db));
+        const int k = klay(c.lane(), rr);
+        if (k >= 1) {
+          sa[k] = a[rr].x;
+          sb[k] = a[rr].y;
         }
-        a[rr] = w;
       }
-      dst_inv(a, sl, tw2, tw32, lane, half_c);
+    }
+  }
+  gsync(c.sy);
+  {  // column pass: WV[:, own columns] = Sy diag(1/d) Sy SR
+    for (int j = c.warp(); j < NP; j += WARPS) {
+      const int o = c.lane();
+      const double v = __ldcg(c.SR() + j * NP + c.C0() + o);
+      if (o < H)
+        slots[(o + 1) * SLOT + j].x = v;
+      else
+        slots[(o - H + 1) * SLOT + j].y = v;
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int h = 0; h < PPW; ++h) {
+      const int q = c.warp() + WARPS * h;
+      double2* sl = slots + (q + 1) * SLOT;
+      double2 a[16];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) a[m] = sl[c.lane() + 32 * m];
+      dst_fwd(a, sl, TW2(), TW32(), c.lane(), HALF_C);
+      const double2* di = c.DI() + q * 16 * 32 + c.lane();
+#pragma unroll
+      for (int rr = 0; rr < 16; ++rr) {
+        const double2 d = __ldcg(di + rr * 32);
+        a[rr] = make_double2(a[rr].x * d.x, a[rr].y * d.y);
+      }
+      dst_inv(a, sl, TW2(), TW32(), c.lane(), HALF_C);
       __syncwarp();
 #pragma unroll
-      for (int m = 0; m < 8; ++m) sl[lane + 32 * m] = a[m];
-      __syncthreads();
-      for (int idx = tid; idx < NP * RS; idx += THREADS) {
-        const int j = idx / RS, o = idx % RS;
-        const double2 t = slots[(o < H ? o + 1 : o - H + 1) * SLOT + j];
-        WV[j * NP + C0 + o] = o < H ? t.x : t.y;
-      }
+      for (int m = 0; m < 8; ++m) sl[c.lane() + 32 * m] = a[m];
     }
-    gsync(sy);
-    {  // z[own rows] = Sx WV[own rows]
-      double2 a[16];
-      const int ja = own_j(0), jb = own_j(1);
-#pragma unroll
-      for (int rr = 0; rr < 16; ++rr) {
-        const int k = klay(lane, rr);
-        double2 w = make_double2(0.0, 0.0);
-        if (k >= 1 && k <= 255)
-          w = make_double2(__ldcg(WV + ja * NP + k - 1), __ldcg(WV + jb * NP + k - 1));
-        else if (k >= 257)
-          w = make_double2(-__ldcg(WV + ja * NP + 511 - k), -__ldcg(WV + jb * NP + 511 - k));
-        a[rr] = w;
-      }
-      dst_inv(a, slots + warp * SLOT, tw2, tw32, lane, half_c);
-#pragma unroll
-      for (int m = 0; m < 8; ++m) {
-        z[0][m] = valid(ja, own_i(m)) ? a[m].x : 0.0;
-        z[1][m] = valid(jb, own_i(m)) ? a[m].y : 0.0;
-      }
+    __syncthreads();
+    for (int j = c.warp(); j < NP; j += WARPS) {
+      const int o = c.lane();
+      const double2 t = slots[(o < H ? o + 1 : o - H + 1) * SLOT + j];
+      c.WV()[j * NP + c.C0() + o] = o < H ? t.x : t.y;
     }
-  };
+  }
+  gsync(c.sy);
+#pragma unroll 1
+  for (int h = 0; h < PPW; ++h) {  // z[own rows] = Sx WV[own rows]
+    double2 a[16];
+    const double* wa = c.WV() + own_j(c, 2 * h) * NP;
+    const double* wb = c.WV() + own_j(c, 2 * h + 1) * NP;
+#pragma unroll
+    for (int rr = 0; rr < 16; ++rr) {
+      const int k = klay(c.lane(), rr);
+      double2 w = make_double2(0.0, 0.0);
+      if (k >= 1 && k <= 255)
+        w = make_double2(__ldcg(wa + k - 1), __ldcg(wb + k - 1));
+      else if (k >= 257)
+        w = make_double2(-__ldcg(wa + 511 - k), -__ldcg(wb + 511 - k));
+      a[rr] = w;
+    }
+    dst_inv(a, slots + (c.warp() + WARPS * h) * SLOT, TW2(), TW32(), c.lane(), HALF_C);
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      z[2 * h][m] = own_valid(c, 2 * h, m) ? a[m].x : 0.0;
+      z[2 * h + 1][m] = own_valid(c, 2 * h + 1, m) ? a[m].y : 0.0;
+    }
+  }
+}
 
-  auto put_pv = [&](const double (&v)[2][8]) {
-    RM_OWN_FOR { PV[own_j(p) * NP + own_i(m)] = v[p][m]; }
-  };
+__device__ __forceinline__ void put_pv(Ctx& c, const double (&v)[NOWN][8]) {
+  RM_OWN_FOR { c.PV()[own_e(c, p, m)] = v[p][m]; }
+}
+
+// p = z (PRE) or r into PV after the reduction of r.z (every CTA is then past its PV reads); returns r.z
+template <bool PRE>
+__device__ __forceinline__ double start_direction(Ctx& c, double s, int64_t& npc) {
+  double r0[NOWN][8], z[NOWN][8];
+  RM_OWN_FOR { r0[p][m] = __ldcg(c.RV() + own_e(c, p, m)); }
+  double pr[1] = {0.0};
+  if constexpr (PRE) {
+    precond(c, r0, z, s);
+    ++npc;
+    RM_OWN_FOR { r0[p][m] = __ldcg(c.RV() + own_e(c, p, m)); }  // (not kept live across the transforms)
+    RM_OWN_FOR { pr[0] += r0[p][m] * z[p][m]; }
+  } else {
+    RM_OWN_FOR {
+      z[p][m] = r0[p][m];
+      pr[0] += r0[p][m] * r0[p][m];
+    }
+  }
+  double o[1];
+  creduce<1>(c, pr, o);
+  put_pv(c, z);
+  gsync(c.sy);
+  return o[0];
+}
+
+}  // namespace fft
+
+template <bool PRE>
+__global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid_constant__ ChainArgs P) {
+  using namespace fft;
+  Ctx c;
+  c.P = &P;
+  c.rank = blockIdx.x % G;
+  const int cid = blockIdx.x / G;
+  const int tid = threadIdx.x;
+  c.sy.gbar = P.gbar + (size_t)cid * 32;
+  c.sy.gred = P.gbuf + (size_t)cid * 1024;
+  c.sy.sched = reinterpret_cast<int*>(c.sy.gred + 8 * G);
+  c.sy.epoch = 0;
+  c.buf = 0;
+  {
+    double2* tw2 = const_cast<double2*>(TW2());    // tw2[q * 32 + t] = W512^{q t}
+    double2* tw32 = const_cast<double2*>(TW32());  // W32^r = W512^{16 r}
+    double2* sym = const_cast<double2*>(SYM());    // 6 stiffness spectra in k-layout
+    for (int i = tid; i < L; i += THREADS) {
+      const int q = i >> 5, t = i & 31;
+      double sn, cs;
+      sincospi(-2.0 * (double)(q * t) / (double)L, &sn, &cs);
+      tw2[i] = make_double2(cs, sn);
+    }
+    if (tid < 16) {
+      double sn, cs;
+      sincospi(-2.0 * (double)(16 * tid) / (double)L, &sn, &cs);
+      tw32[tid] = make_double2(cs, sn);
+    }
+    for (int i = tid; i < 6 * L; i += THREADS) sym[i] = P.fsym[i];
+  }
+  const rm_sweep& W_ = P.sw;
+  constexpr int nx = NX;
+  c.di_s = __longlong_as_double(0x7ff8000000000000ll);  // NaN: nothing cached
+  const int64_t max_iter = W_.max_iter > 0 ? W_.max_iter : 10 * (int64_t)NX * NX;
+  const bool need_in = W_.explicit_rhs || W_.x0_mode == 1;
+  c.base = P.fscratch + (size_t)cid * (NVEC * VEC + G * DIV);
+  // zero this chain slot's vectors once (padding row / column 255 is never written afterwards)
+  for (size_t i = (size_t)c.rank * THREADS + tid; i < NVEC * VEC; i += (size_t)G * THREADS) c.base[i] = 0.0;
+  gsync(c.sy);
 
   for (;;) {
-    if (rank == 0 && tid == 0) sy.sched[0] = atomicAdd(P.chain_counter, 1);
-    gsync(sy);
-    const int chain = __ldcg(sy.sched);
-    gsync(sy);
+    if (c.rank == 0 && tid == 0) c.sy.sched[0] = atomicAdd(P.chain_counter, 1);
+    gsync(c.sy);
+    const int chain = __ldcg(c.sy.sched);
+    gsync(c.sy);
     if (chain >= W_.nchains) break;
     const int n0 = W_.first + chain * W_.cstride;
     const int n1 = min(n0 + W_.clen - 1, W_.nmax);
@@ -554,142 +676,152 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const ChainA
       const bool rhs_ain = need_in && W_.explicit_rhs && !in_tile && n >= 2 && W_.d_ain != nullptr &&
                            W_.d_hg != nullptr && !rhs_free;
       int64_t nmv = 0, npc = 0;
-      double acc[2][8];
+      double acc[NOWN][8];
       RM_OWN_FOR { acc[p][m] = 0.0; }
       if (need_in && !in_tile) {
         const double* src = W_.d_src + (int64_t)(n - 1) * W_.src_stride;
-        RM_OWN_FOR {
-          const int j = own_j(p), i = own_i(m);
-          PV[j * NP + i] = valid(j, i) ? __ldcg(src + j * nx + i) : 0.0;
-        }
-        gsync(sy);
+        double v[NOWN][8];
+        RM_OWN_FOR { v[p][m] = own_valid(c, p, m) ? __ldcg(src + own_j(c, p) * nx + own_i(c, m)) : 0.0; }
+        put_pv(c, v);
+        gsync(c.sy);
       }
+      double mv[NOWN][8];  // M v of the step input (explicit sides without an apply, x0 = v)
+      if (rhs_free || rhs_ain) mass_own(c, mv);
       if (rhs_free) {
         const double* Hn = W_.d_hg + (int64_t)(n - 1) * W_.hg_stride;
         const double q = s / s_prev;
+        double bv[NOWN][8], rv[NOWN][8], hv[NOWN][8];
         RM_OWN_FOR {
-          const int j = own_j(p), i = own_i(m);
-          if (valid(j, i)) {
-            const int e = j * NP + i;
-            acc[p][m] = (1.0 + q) * mass_pv(j, i) - q * (__ldcg(BV + e) - __ldcg(RV + e) + __ldcg(Hn + j * nx + i));
-          }
+          const int e = own_e(c, p, m);
+          const bool ok = own_valid(c, p, m);
+          bv[p][m] = __ldcg(c.BV() + e);
+          rv[p][m] = __ldcg(c.RV() + e);
+          hv[p][m] = ok ? __ldcg(Hn + own_j(c, p) * nx + own_i(c, m)) : 0.0;
+        }
+        RM_OWN_FOR {
+          acc[p][m] = own_valid(c, p, m) ? (1.0 + q) * mv[p][m] - q * (bv[p][m] - rv[p][m] + hv[p][m]) : 0.0;
         }
       } else if (rhs_ain) {
         const double* An = W_.d_ain + (int64_t)(n - 1) * W_.ain_stride;
         const double* Hn = W_.d_hg + (int64_t)(n - 1) * W_.hg_stride;
         const double q = s / (0.5 * W_.d_dt[n - 2]);
+        double av[NOWN][8], hv[NOWN][8];
         RM_OWN_FOR {
-          const int j = own_j(p), i = own_i(m);
-          if (valid(j, i)) {
-            const int gi = j * nx + i;
-            acc[p][m] = (1.0 + q) * mass_pv(j, i) - q * (__ldcg(An + gi) + __ldcg(Hn + gi));
-          }
+          const int gi = own_j(c, p) * nx + own_i(c, m);
+          const bool ok = own_valid(c, p, m);
+          av[p][m] = ok ? __ldcg(An + gi) : 0.0;
+          hv[p][m] = ok ? __ldcg(Hn + gi) : 0.0;
         }
+        RM_OWN_FOR { acc[p][m] = own_valid(c, p, m) ? (1.0 + q) * mv[p][m] - q * (av[p][m] + hv[p][m]) : 0.0; }
       } else if (need_in) {
-        apply_pv(acc, -s);  // (M - s K) v
+        apply_pv(c, acc, -s);  // (M - s K) v
         nmv = 1;
+        if (W_.x0_mode == 1) mass_own(c, mv);
+      } else if (W_.x0_mode == 1) {
+        mass_own(c, mv);
       }
       s_prev = s;
       chain_ok = false;
 
       // right-hand side, initial iterate and residual
       double part[2] = {0.0, 0.0};
-      RM_OWN_FOR {
-        const int j = own_j(p), i = own_i(m);
-        const int e = j * NP + i;
-        double b = 0.0, x = 0.0, r = 0.0;
-        if (valid(j, i)) {
-          const double am = acc[p][m];
-          if (W_.explicit_rhs) b = am;
-          if (Fn) {
-            const double f = fs * __ldcg(Fn + j * nx + i);
-            b = W_.explicit_rhs ? f + b : f;
-          }
-          if (W_.x0_mode == 1) {
-            x = __ldcg(PV + e);
-            r = b - (2.0 * mass_pv(j, i) - am);  // (M + s K) v = 2 M v - (M - s K) v
-          } else {
-            r = b;
-          }
+      {
+        double fv[NOWN][8], xv[NOWN][8];
+        RM_OWN_FOR {
+          const bool ok = own_valid(c, p, m);
+          fv[p][m] = (Fn && ok) ? __ldcg(Fn + own_j(c, p) * nx + own_i(c, m)) : 0.0;
+          xv[p][m] = (W_.x0_mode == 1 && ok) ? __ldcg(c.PV() + own_e(c, p, m)) : 0.0;
         }
-        BV[e] = b;
-        XV[e] = x;
-        RV[e] = r;
-        part[0] += b * b;
-        part[1] += r * r;
+        RM_OWN_FOR {
+          const int e = own_e(c, p, m);
+          double b = 0.0, r = 0.0;
+          if (own_valid(c, p, m)) {
+            const double am = acc[p][m];
+            if (W_.explicit_rhs) b = am;
+            if (Fn) b = W_.explicit_rhs ? fs * fv[p][m] + b : fs * fv[p][m];
+            // x0 = v: (M + s K) v = 2 M v - (M - s K) v
+            r = W_.x0_mode == 1 ? b - (2.0 * mv[p][m] - am) : b;
+          }
+          c.BV()[e] = b;
+          c.XV()[e] = xv[p][m];
+          c.RV()[e] = r;
+          part[0] += b * b;
+          part[1] += r * r;
+        }
       }
       if (W_.x0_mode == 2 || W_.x0_mode == 4) {
         // given initial iterate (x0_mode 2, stepper.py:203) / apply probe (x0_mode 4: out = (M + s K) b)
-        gsync(sy);  // every CTA done reading PV
+        gsync(c.sy);  // every CTA done reading PV
         const double* x0 = W_.x0_mode == 2 ? W_.d_x0 + (int64_t)n * W_.x0_stride : Fn;
         const double sc = W_.x0_mode == 2 ? 1.0 : fs;
-        RM_OWN_FOR {
-          const int j = own_j(p), i = own_i(m);
-          PV[j * NP + i] = valid(j, i) ? sc * __ldcg(x0 + j * nx + i) : 0.0;
-        }
-        gsync(sy);
-        apply_pv(acc, s);
+        double v[NOWN][8];
+        RM_OWN_FOR { v[p][m] = own_valid(c, p, m) ? sc * __ldcg(x0 + own_j(c, p) * nx + own_i(c, m)) : 0.0; }
+        put_pv(c, v);
+        gsync(c.sy);
+        apply_pv(c, acc, s);
         ++nmv;
         part[1] = 0.0;
         RM_OWN_FOR {
-          const int j = own_j(p), i = own_i(m);
-          const int e = j * NP + i;
+          const int e = own_e(c, p, m);
           if (W_.x0_mode == 4) {
-            XV[e] = acc[p][m];
+            c.XV()[e] = acc[p][m];
           } else {
-            const double r = valid(j, i) ? __ldcg(BV + e) - acc[p][m] : 0.0;
-            XV[e] = valid(j, i) ? __ldcg(PV + e) : 0.0;
-            RV[e] = r;
+            const double r = own_valid(c, p, m) ? __ldcg(c.BV() + e) - acc[p][m] : 0.0;
+            c.XV()[e] = v[p][m];
+            c.RV()[e] = r;
             part[1] += r * r;
           }
         }
       }
       double tot[2];
-      greduce<2>(part, wred, sy, buf, rank, warp, lane, tot);
+      creduce<2>(c, part, tot);
       const double bnorm = sqrt(tot[0]);
       const double target = bnorm > 0.0 ? W_.rel_tol * bnorm : W_.rel_tol;
       if (W_.d_guess && W_.x0_mode < 3 && sqrt(tot[1]) > target) {
         const double* gu = W_.d_guess + (int64_t)n * W_.guess_stride;
         const double* Gr = W_.d_gadd ? W_.d_gadd + (int64_t)n * W_.gadd_stride : nullptr;
         const double* Ax0 = W_.d_gax ? W_.d_gax + (int64_t)n * W_.gax_stride : nullptr;
-        double ag[2][8];
-        if (!Ax0) {
-          gsync(sy);  // every CTA done reading PV
+        auto guess_vec = [&](double (&g0)[NOWN][8]) {
           RM_OWN_FOR {
-            const int j = own_j(p), i = own_i(m);
             double v = 0.0;
-            if (valid(j, i)) {
-              const int gi = j * nx + i;
+            if (own_valid(c, p, m)) {
+              const int gi = own_j(c, p) * nx + own_i(c, m);
               v = Gr ? __ldcg(gu + gi) - __ldcg(Gr + gi) : __ldcg(gu + gi);
             }
-            PV[j * NP + i] = v;
+            g0[p][m] = v;
           }
-          gsync(sy);
-          apply_pv(ag, s);
+        };
+        double ag[NOWN][8];
+        if (!Ax0) {
+          double g0[NOWN][8];
+          guess_vec(g0);
+          gsync(c.sy);  // every CTA done reading PV
+          put_pv(c, g0);
+          gsync(c.sy);
+          apply_pv(c, ag, s);
           ++nmv;
+        } else {
+          RM_OWN_FOR { ag[p][m] = own_valid(c, p, m) ? __ldcg(Ax0 + own_j(c, p) * nx + own_i(c, m)) : 0.0; }
         }
         double pg[1] = {0.0};
         RM_OWN_FOR {
-          const int j = own_j(p), i = own_i(m);
-          double r = 0.0;
-          if (valid(j, i)) r = __ldcg(BV + j * NP + i) - (Ax0 ? __ldcg(Ax0 + j * nx + i) : ag[p][m]);
+          const double r = own_valid(c, p, m) ? __ldcg(c.BV() + own_e(c, p, m)) - ag[p][m] : 0.0;
           ag[p][m] = r;
           pg[0] += r * r;
         }
         double rg[1];
-        greduce<1>(pg, wred, sy, buf, rank, warp, lane, rg);
+        creduce<1>(c, pg, rg);
         if (rg[0] < tot[1]) {
           tot[1] = rg[0];
+          double g0[NOWN][8];
+          if (Ax0)
+            guess_vec(g0);
+          else
+            RM_OWN_FOR { g0[p][m] = __ldcg(c.PV() + own_e(c, p, m)); }
           RM_OWN_FOR {
-            const int j = own_j(p), i = own_i(m);
-            const int e = j * NP + i;
-            double x0 = 0.0;
-            if (valid(j, i)) {
-              const int gi = j * nx + i;
-              x0 = Ax0 ? (Gr ? __ldcg(gu + gi) - __ldcg(Gr + gi) : __ldcg(gu + gi)) : __ldcg(PV + e);
-            }
-            XV[e] = x0;
-            RV[e] = ag[p][m];
+            const int e = own_e(c, p, m);
+            c.XV()[e] = g0[p][m];
+            c.RV()[e] = ag[p][m];
           }
         }
       }
@@ -701,75 +833,61 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const ChainA
       if (W_.x0_mode == 3) {
         // preconditioner probe: x = P^-1 b
         if constexpr (PRE) {
-          double r0[2][8], z[2][8];
-          RM_OWN_FOR { r0[p][m] = __ldcg(RV + own_j(p) * NP + own_i(m)); }
-          precond(r0, z, s);
+          double r0[NOWN][8], z[NOWN][8];
+          RM_OWN_FOR { r0[p][m] = __ldcg(c.RV() + own_e(c, p, m)); }
+          precond(c, r0, z, s);
           ++npc;
-          RM_OWN_FOR { XV[own_j(p) * NP + own_i(m)] = z[p][m]; }
+          RM_OWN_FOR { c.XV()[own_e(c, p, m)] = z[p][m]; }
         }
         done = true;
       }
+      if (!done) rz = start_direction<PRE>(c, s, npc);
 
-      // p = z (PRE) or r into PV, after every CTA finished reading PV
-      auto start_direction = [&]() {
-        double r0[2][8], z[2][8];
-        RM_OWN_FOR { r0[p][m] = __ldcg(RV + own_j(p) * NP + own_i(m)); }
-        double pr[1] = {0.0};
-        if constexpr (PRE) {
-          precond(r0, z, s);
-          ++npc;
-          RM_OWN_FOR { pr[0] += r0[p][m] * z[p][m]; }
-        } else {
-          RM_OWN_FOR {
-            z[p][m] = r0[p][m];
-            pr[0] += r0[p][m] * r0[p][m];
-          }
-        }
-        double o[1];
-        greduce<1>(pr, wred, sy, buf, rank, warp, lane, o);  // also: every CTA is past its PV reads
-        rz = o[0];
-        put_pv(z);
-        gsync(sy);
-      };
-      if (!done) start_direction();
-
+      // PCG (krylov.py:57-86 with the tau preconditioner); x += alpha p is folded into the next direction
+      // update (or the acceptance check), which reads p anyway
+      double alpha = 0.0;
       for (int64_t k = 1; !done; ++k) {
         if (k > max_iter) {
           fail = RM_CG_BUDGET;
           its = max_iter;
           break;
         }
-        double ap[2][8];
-        apply_pv(ap, s);
+        double ap[NOWN][8];
+        apply_pv(c, ap, s);
         ++nmv;
         double p1[1] = {0.0};
-        RM_OWN_FOR { p1[0] += __ldcg(PV + own_j(p) * NP + own_i(m)) * ap[p][m]; }
+        {
+          double pv[NOWN][8];
+          RM_OWN_FOR { pv[p][m] = __ldcg(c.PV() + own_e(c, p, m)); }
+          RM_OWN_FOR { p1[0] += pv[p][m] * ap[p][m]; }
+        }
         double pap[1];
-        greduce<1>(p1, wred, sy, buf, rank, warp, lane, pap);
+        creduce<1>(c, p1, pap);
         if (!isfinite(pap[0]) || pap[0] <= 0.0) {
           fail = RM_CG_BREAKDOWN;
           its = k;
           break;
         }
-        const double alpha = rz / pap[0];
-        double rn[2][8];
-        RM_OWN_FOR {
-          const int e = own_j(p) * NP + own_i(m);
-          XV[e] = __ldcg(XV + e) + alpha * __ldcg(PV + e);
-          rn[p][m] = __ldcg(RV + e) - alpha * ap[p][m];
-          RV[e] = rn[p][m];
+        alpha = rz / pap[0];
+        double rn[NOWN][8];
+        {
+          double rv[NOWN][8];
+          RM_OWN_FOR { rv[p][m] = __ldcg(c.RV() + own_e(c, p, m)); }
+          RM_OWN_FOR {
+            rn[p][m] = rv[p][m] - alpha * ap[p][m];
+            c.RV()[own_e(c, p, m)] = rn[p][m];
+          }
         }
         double red2[2];
-        double z[2][8];
+        double z[NOWN][8];
         {
           double part2[2] = {0.0, 0.0};
           if constexpr (PRE) {
-            precond(rn, z, s);
+            RM_OWN_FOR { part2[0] += rn[p][m] * rn[p][m]; }
+            precond(c, rn, z, s);
             ++npc;
-            RM_OWN_FOR {
-              part2[0] += rn[p][m] * rn[p][m];
-              part2[1] += rn[p][m] * z[p][m];
-            }
+            RM_OWN_FOR { rn[p][m] = __ldcg(c.RV() + own_e(c, p, m)); }  // (not kept live across the transforms)
+            RM_OWN_FOR { part2[1] += rn[p][m] * z[p][m]; }
           } else {
             RM_OWN_FOR {
               z[p][m] = rn[p][m];
@@ -777,7 +895,7 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const ChainA
             }
             part2[1] = part2[0];
           }
-          greduce<2>(part2, wred, sy, buf, rank, warp, lane, red2);
+          creduce<2>(c, part2, red2);
         }
         res = sqrt(red2[0]);
         if (!isfinite(res)) {
@@ -786,25 +904,39 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const ChainA
           break;
         }
         if (res <= target) {
-          // acceptance on the true residual (krylov.py:71-83); every CTA is past its PV reads
-          double xv[2][8];
-          RM_OWN_FOR { xv[p][m] = __ldcg(XV + own_j(p) * NP + own_i(m)); }
-          put_pv(xv);
-          gsync(sy);
-          double ax[2][8];
-          apply_pv(ax, s);
+          // x += alpha p, then acceptance on the true residual (krylov.py:71-83); every CTA is past its PV
+          // reads (the reductions above were group barriers)
+          double xv[NOWN][8];
+          {
+            double xo[NOWN][8], pv[NOWN][8];
+            RM_OWN_FOR {
+              xo[p][m] = __ldcg(c.XV() + own_e(c, p, m));
+              pv[p][m] = __ldcg(c.PV() + own_e(c, p, m));
+            }
+            RM_OWN_FOR {
+              xv[p][m] = xo[p][m] + alpha * pv[p][m];
+              c.XV()[own_e(c, p, m)] = xv[p][m];
+            }
+          }
+          put_pv(c, xv);
+          gsync(c.sy);
+          double ax[NOWN][8];
+          apply_pv(c, ax, s);
           ++nmv;
           double pt[1] = {0.0};
-          RM_OWN_FOR {
-            const int j = own_j(p), i = own_i(m);
-            const double rt = valid(j, i) ? __ldcg(BV + j * NP + i) - ax[p][m] : 0.0;
-            ax[p][m] = rt;
-            pt[0] += rt * rt;
+          {
+            double bv[NOWN][8];
+            RM_OWN_FOR { bv[p][m] = __ldcg(c.BV() + own_e(c, p, m)); }
+            RM_OWN_FOR {
+              const double rt = own_valid(c, p, m) ? bv[p][m] - ax[p][m] : 0.0;
+              ax[p][m] = rt;
+              pt[0] += rt * rt;
+            }
           }
           double tt[1];
-          greduce<1>(pt, wred, sy, buf, rank, warp, lane, tt);
+          creduce<1>(c, pt, tt);
           const double true_res = sqrt(tt[0]);
-          RM_OWN_FOR { RV[own_j(p) * NP + own_i(m)] = ax[p][m]; }
+          RM_OWN_FOR { c.RV()[own_e(c, p, m)] = ax[p][m]; }
           if (true_res <= fmax(target, 10.0 * res)) {
             its = k;
             done = true;
@@ -816,33 +948,41 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const ChainA
             done = true;
             break;
           }
-          start_direction();
+          rz = start_direction<PRE>(c, s, npc);
           continue;
         }
         const double beta = red2[1] / rz;
         rz = red2[1];
-        // p = z + beta p (every CTA finished reading PV: the reductions above were group barriers)
-        RM_OWN_FOR {
-          const int e = own_j(p) * NP + own_i(m);
-          PV[e] = z[p][m] + beta * __ldcg(PV + e);
+        // x += alpha p, p = z + beta p (every CTA finished reading PV: the reductions were group barriers)
+        {
+          double xo[NOWN][8], pv[NOWN][8];
+          RM_OWN_FOR {
+            xo[p][m] = __ldcg(c.XV() + own_e(c, p, m));
+            pv[p][m] = __ldcg(c.PV() + own_e(c, p, m));
+          }
+          RM_OWN_FOR {
+            const int e = own_e(c, p, m);
+            c.XV()[e] = xo[p][m] + alpha * pv[p][m];
+            c.PV()[e] = z[p][m] + beta * pv[p][m];
+          }
         }
-        gsync(sy);
+        gsync(c.sy);
       }
 
       chain_ok = done && !fail && W_.x0_mode < 3;
-      if (rank == 0 && tid == 0) {
+      if (c.rank == 0 && tid == 0) {
         atomicAdd(W_.d_counters, 1ull);
         atomicAdd(W_.d_counters + 1, (unsigned long long)its);
         atomicAdd(W_.d_counters + 2, (unsigned long long)nmv);
         atomicAdd(W_.d_counters + 3, (unsigned long long)npc);
       }
       if (fail) {
-        if (rank == 0 && tid == 0 && atomicCAS(P.fail, 0, fail) == 0) {
+        if (c.rank == 0 && tid == 0 && atomicCAS(P.fail, 0, fail) == 0) {
           P.fail_info[0] = (double)n;
           P.fail_info[1] = (double)its;
           P.fail_info[2] = res;
         }
-        gsync(sy);
+        gsync(c.sy);
         break;
       }
       // ---------------- MGRIT epilogue: y = [G_n +] x [- S_n] ----------------
@@ -853,29 +993,40 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const ChainA
       double* On = W_.d_out ? W_.d_out + (int64_t)oi * W_.out_stride : nullptr;
       double* Kn = W_.d_keep ? W_.d_keep + (int64_t)oi * W_.keep_stride : nullptr;
       double* An = W_.d_ax ? W_.d_ax + (int64_t)oi * W_.ax_stride : nullptr;
-      gsync(sy);  // every CTA done reading PV before it is overwritten with y
+      gsync(c.sy);  // every CTA done reading PV before it is overwritten with y
       double py[1] = {0.0};
-      RM_OWN_FOR {
-        const int j = own_j(p), i = own_i(m);
-        if (valid(j, i)) {
-          const int gi = j * nx + i, e = j * NP + i;
-          double y = __ldcg(XV + e);
-          if (An) An[gi] = __ldcg(BV + e) - __ldcg(RV + e);  // A x = b - r (true residual)
-          if (Gn) y = __ldcg(Gn + gi) + y;
-          if (Kn) Kn[gi] = y;
-          if (Sn) y = y - __ldcg(Sn + gi);
-          if (On) On[gi] = y;
-          if (next_in_tile) PV[e] = y;
-          py[0] += y * y;
+      {
+        double xv[NOWN][8], gv[NOWN][8], sv[NOWN][8], bv[NOWN][8], rv[NOWN][8];
+        RM_OWN_FOR {
+          const bool ok = own_valid(c, p, m);
+          const int e = own_e(c, p, m), gi = own_j(c, p) * nx + own_i(c, m);
+          xv[p][m] = __ldcg(c.XV() + e);
+          gv[p][m] = (Gn && ok) ? __ldcg(Gn + gi) : 0.0;
+          sv[p][m] = (Sn && ok) ? __ldcg(Sn + gi) : 0.0;
+          bv[p][m] = An ? __ldcg(c.BV() + e) : 0.0;
+          rv[p][m] = An ? __ldcg(c.RV() + e) : 0.0;
+        }
+        RM_OWN_FOR {
+          if (own_valid(c, p, m)) {
+            const int gi = own_j(c, p) * nx + own_i(c, m);
+            double y = xv[p][m];
+            if (An) An[gi] = bv[p][m] - rv[p][m];  // A x = b - r (true residual)
+            if (Gn) y = gv[p][m] + y;
+            if (Kn) Kn[gi] = y;
+            if (Sn) y = y - sv[p][m];
+            if (On) On[gi] = y;
+            if (next_in_tile) c.PV()[own_e(c, p, m)] = y;
+            py[0] += y * y;
+          }
         }
       }
       if (W_.d_norms) {
         double yy[1];
-        greduce<1>(py, wred, sy, buf, rank, warp, lane, yy);
-        if (rank == 0 && tid == 0) W_.d_norms[oi] = yy[0];
+        creduce<1>(c, py, yy);
+        if (c.rank == 0 && tid == 0) W_.d_norms[oi] = yy[0];
       }
       in_tile = next_in_tile;
-      gsync(sy);
+      gsync(c.sy);
     }
   }
 }
@@ -913,7 +1064,7 @@ bool fft_supported(int np, int nx, int ny) { return np == fft::NP && nx == fft::
 
 int fft_group() { return fft::G; }
 
-size_t fft_scratch_doubles_per_chain() { return fft::NVEC * fft::VEC; }
+size_t fft_scratch_doubles_per_chain() { return fft::NVEC * fft::VEC + fft::G * fft::DIV; }
 
 static cudaError_t fft_prepare(const void* kern) {
   return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fft::SMEM);
