@@ -48,7 +48,8 @@ constexpr int WARPS = 16;
 constexpr int NOWN = 2;               // owner rows per thread (one packed pair per warp)
 constexpr int PPW = NOWN / 2;          // packed pairs per warp
 constexpr int NSLOT = H + 2;          // packed pairs incl. the +-1 halo
-constexpr int SLOT = 548;             // double2 per slot: >= 16 x 34 transpose scratch
+constexpr int SLOT = 545;             // double2 per slot: >= 16 x 34 transpose scratch; = 1 mod 8 (16-byte
+                                      // accesses to consecutive slots hit distinct bank groups)
 constexpr int TS = 34;                // transpose row stride (conflict-free 16-byte accesses)
 constexpr int NVEC = 6;               // per-chain vectors
 constexpr size_t VEC = (size_t)NP * NP;
@@ -265,13 +266,9 @@ __device__ __forceinline__ void greduce(double (&part)[NV], double* wred, Sync& 
     }
   }
   gsync(sy);
+  // every warp sums the G tile partials with the same butterfly: identical in all CTAs
 #pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    double x = 0.0;
-#pragma unroll
-    for (int q = 0; q < G; ++q) x += __ldcg(sy.gred + (buf * 4 + v) * G + q);
-    out[v] = x;
-  }
+  for (int v = 0; v < NV; ++v) out[v] = warp_allsum(lane < G ? __ldcg(sy.gred + (buf * 4 + v) * G + lane) : 0.0);
   buf ^= 1;
 }
 
@@ -349,18 +346,12 @@ __device__ __forceinline__ void col_pass_apply(Ctx& c) {
   double2* slots = SLOTS();
   // stage columns C0-1 .. C0+32 into slots s = 0..17 (pair (C0+s-1, C0+s+15)), natural row order; a warp
   // covers 34 consecutive columns of one row per step (coalesced)
-  for (int j = c.warp(); j < NP; j += WARPS) {
-    const double* row = c.PV() + j * NP + c.C0();
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {  // the strip's 34 columns: two passes of the warp
-      const int o = c.lane() + 32 * h - 1;
-      if (o <= 32) {
-        const int col = c.C0() + o;
-        const double v = (col >= 0 && col < NP) ? __ldcg(row + o) : 0.0;
-        if (o <= 16) slots[(o + 1) * SLOT + j].x = v;
-        if (o >= 15) slots[(o - 15) * SLOT + j].y = v;
-      }
-    }
+  // stage columns C0-1 .. C0+32: slot s = (column C0+s-1, column C0+s+15), one 16-byte store per element pair
+  for (int idx = c.tid(); idx < NP * NSLOT; idx += THREADS) {
+    const int j = idx / NSLOT, s = idx - j * NSLOT;
+    const int ca = c.C0() + s - 1, cb = c.C0() + s + H - 1;
+    const double* row = c.PV() + j * NP;
+    slots[s * SLOT + j] = make_double2(ca >= 0 ? __ldcg(row + ca) : 0.0, cb < NP ? __ldcg(row + cb) : 0.0);
   }
   for (int idx = c.tid(); idx < NSLOT * (L - NP); idx += THREADS)
     slots[(idx / (L - NP)) * SLOT + NP + idx % (L - NP)] = make_double2(0.0, 0.0);
@@ -402,10 +393,11 @@ __device__ __forceinline__ void col_pass_apply(Ctx& c) {
   }
   __syncthreads();
   // store the 32 own columns, one row per warp step
-  for (int j = c.warp(); j < NP; j += WARPS) {
-    const int o = c.lane();
-    const double2 t = slots[(o < H ? o + 1 : o - H + 1) * SLOT + j];
-    c.WV()[j * NP + c.C0() + o] = o < H ? t.x : t.y;
+  for (int idx = c.tid(); idx < NP * H; idx += THREADS) {
+    const int j = idx / H, q = idx % H;
+    const double2 t = slots[(q + 1) * SLOT + j];
+    c.WV()[j * NP + c.C0() + q] = t.x;
+    c.WV()[j * NP + c.C0() + q + H] = t.y;
   }
 }
 
@@ -526,13 +518,10 @@ __device__ __forceinline__ void precond(Ctx& c, const double (&r)[NOWN][8], doub
   }
   gsync(c.sy);
   {  // column pass: WV[:, own columns] = Sy diag(1/d) Sy SR
-    for (int j = c.warp(); j < NP; j += WARPS) {
-      const int o = c.lane();
-      const double v = __ldcg(c.SR() + j * NP + c.C0() + o);
-      if (o < H)
-        slots[(o + 1) * SLOT + j].x = v;
-      else
-        slots[(o - H + 1) * SLOT + j].y = v;
+    for (int idx = c.tid(); idx < NP * H; idx += THREADS) {
+      const int j = idx / H, q = idx % H;
+      const double* row = c.SR() + j * NP + c.C0();
+      slots[(q + 1) * SLOT + j] = make_double2(__ldcg(row + q), __ldcg(row + q + H));
     }
     __syncthreads();
 #pragma unroll 1
@@ -555,10 +544,11 @@ __device__ __forceinline__ void precond(Ctx& c, const double (&r)[NOWN][8], doub
       for (int m = 0; m < 8; ++m) sl[c.lane() + 32 * m] = a[m];
     }
     __syncthreads();
-    for (int j = c.warp(); j < NP; j += WARPS) {
-      const int o = c.lane();
-      const double2 t = slots[(o < H ? o + 1 : o - H + 1) * SLOT + j];
-      c.WV()[j * NP + c.C0() + o] = o < H ? t.x : t.y;
+    for (int idx = c.tid(); idx < NP * H; idx += THREADS) {
+      const int j = idx / H, q = idx % H;
+      const double2 t = slots[(q + 1) * SLOT + j];
+      c.WV()[j * NP + c.C0() + q] = t.x;
+      c.WV()[j * NP + c.C0() + q + H] = t.y;
     }
   }
   gsync(c.sy);
