@@ -1,9 +1,11 @@
-"""Benchmark: MGRIT time-to-solution on BASELINE config 2 (127^2 DOF x 4096 steps, multilevel V, m=8).
+"""Benchmark: MGRIT time-to-solution on BASELINE config 3 (255^2 DOF x 16384 steps, multilevel V, m=16) --
+the largest BASELINE configuration that converges on one GPU (config 4's MGRIT diverges in the reference
+itself, tests/test_gpu_regimes.py; config 5 needs 549 GB for U).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2] [--nt NT]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg3] [--nt NT]
 
 One "step" = one complete MGRIT solve (G setup, V-cycles to residual < 1e-8,
-finalisation) of the canonical seeded cfg2 problem.  Prints ONE JSON line.
+finalisation) of the canonical seeded problem.  Prints ONE JSON line.
 
 Arms
   ours       the B200 path.  ``value`` = ndof*Nt / time-to-solution with the
@@ -15,7 +17,17 @@ Arms
              oracle/riesz_oracle.py, numpy/OpenBLAS on all host cores): each step
              times a bounded sample of real propagations at every level's dt and
              extrapolates to the full solve with the reference-equivalent counts
-             (profiles/cfg2_reference_counts.json: identical control flow).
+             (profiles/<config>_reference_counts.json: the product run with the reference's
+             own unpreconditioned CG -- identical control flow and solve counts; its CG counts
+             are pinned against reference runs in the same step regime by
+             tests/test_gpu_regimes.py).
+
+Parity of the timed path: before timing, the benched default solver runs the cfg3 case
+in the full run's step regime (T = 1/16, Nt = 1024) and is checked against the
+reference's own run (tests/golden/cfg3_split.npz: iteration count, solve counts,
+<= 1e-10 per time point); the timed solve's trace is checked against the
+reference-algorithm run of the full config (iteration count, solve counts, residual
+history).  The line carries the outcome ("parity").
 """
 
 from __future__ import annotations
@@ -47,10 +59,13 @@ def dist_env():
     return ws, int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0"))
 
 
+CONFIG_INDEX = {"cfg1": 0, "cfg2": 1, "cfg3": 2, "cfg4": 3, "cfg5": 4}
+
+
 def load_case(args):
-    """The bench workload.  Strong scaling (default): the BASELINE config 2 problem split over the ranks.
-    Weak scaling (option): 4096 fine steps PER GPU over a horizon T = N at the same step -- a different
-    problem whose MGRIT iteration count grows with T (measured 21 / 30 / 90 for T = 1 / 2 / 8)."""
+    """The bench workload: the BASELINE configuration itself (strong scaling: the same problem split over the
+    ranks), or with ``--scaling weak`` Nt * N fine steps over the horizon T = N at the same step (a different
+    problem: MGRIT's iteration count grows with the horizon)."""
     from paper_1805_06688_b200.configs import make_case
 
     ws = dist_env()[0]
@@ -69,12 +84,15 @@ def case_options(case, args):
 def workload(case):
     T = float(case.tmesh.points[-1])
     per = f" (weak scaling: {int(round(T))} x the BASELINE horizon, T = {T:g}, same step)" if T != 1.0 else ""
-    return {"workload": f"BASELINE configs[1] ({case.name}){per}: Riesz SFDE, {case.grid.nx}x{case.grid.ny} DOF, "
-                        f"Nt={case.tmesh.n_intervals} uniform, beta={case.beta}, gamma={case.gamma}, "
-                        f"Kx={case.kx}, Ky={case.ky}, multilevel MGRIT V-cycle m={case.m} FCF, CG tol "
-                        f"{case.cg_rel_tol:g}, halt {case.halt_tol:g}",
+    mesh = "graded (n/Nt)^2" if case.name == "cfg4" else "uniform"
+    levels = "two-level" if case.max_levels == 2 else "multilevel"
+    vec = case.grid.ndof * 8 * (case.tmesh.n_intervals + 1)
+    return {"workload": f"BASELINE configs[{CONFIG_INDEX[case.name]}] ({case.name}){per}: Riesz SFDE, "
+                        f"{case.grid.nx}x{case.grid.ny} DOF, Nt={case.tmesh.n_intervals} {mesh}, beta={case.beta}, "
+                        f"gamma={case.gamma}, Kx={case.kx}, Ky={case.ky}, {levels} MGRIT V-cycle m={case.m} FCF, "
+                        f"CG tol {case.cg_rel_tol:g}, halt {case.halt_tol:g}",
             "ndof": case.grid.ndof, "nt": case.tmesh.n_intervals, "m": case.m,
-            "l2": "inputs larger than L2: U, G and the residual copy are 528 MB each (no flush needed)"}
+            "l2": f"inputs larger than L2: U and G are {vec / 1e9:.2f} GB each (no flush needed)"}
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -135,16 +153,19 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- CPU reference leg
 def reference_counts(case):
-    """Reference-equivalent solve / CG counts of cfg2 (Nt = 4096); for the weak-scaled Nt = 4096 k the
-    counts are scaled by k (solve counts grow linearly with Nt at a fixed MGRIT iteration count; the
-    extra coarse level is not charged) and labelled as such."""
+    """Reference-equivalent solve / CG counts of the configuration at its BASELINE size
+    (profiles/<config>_reference_counts.json); for a weak-scaled Nt = Nt0 k the counts are scaled by k (solve
+    counts grow linearly with Nt at a fixed MGRIT iteration count; the extra coarse level is not charged) and
+    labelled as such."""
+    from paper_1805_06688_b200.configs import CONFIGS
+
     path = os.path.join(PROFILES, f"{case.name}_reference_counts.json")
-    n = case.tmesh.n_intervals
-    if case.name != "cfg2" or n % 4096 or not os.path.exists(path):
+    n, n0 = case.tmesh.n_intervals, CONFIGS[case.name][1]
+    if n % n0 or not os.path.exists(path):
         return None
     with open(path) as f:
         counts = json.load(f)
-    k = n // 4096
+    k = n // n0
     if k > 1:
         scale = lambda d: {key: v * k for key, v in d.items()}  # noqa: E731
         counts = dict(counts, setup=scale(counts["setup"]), levels=[scale(d) for d in counts["levels"]],
@@ -255,19 +276,70 @@ def measure_fp64_peak():
     return 2.0 * n**3 / (best * 1e-3) / 1e12
 
 
-def ncu_traffic():
-    path = os.path.join(PROFILES, "ncu_chain_summary.json")
+def ncu_summary(fft: bool):
+    """DRAM traffic per launch of the dominant kernel from the committed ncu capture summary (profiles/)."""
+    path = os.path.join(PROFILES, "r02_ncu_fft_summary.json" if fft else "ncu_chain_summary.json")
     if os.path.exists(path):
         with open(path) as f:
-            d = json.load(f)
-        return d.get("dram_bytes_per_launch"), d.get("launch")
-    return None, None
+            return json.load(f)
+    return {}
+
+
+def parity_checks(case, opts, trace):
+    """Parity of the timed path against the reference (module docstring).  Returns a dict for the JSON line."""
+    import numpy as np
+
+    from paper_1805_06688_b200.configs import make_case
+    from paper_1805_06688_b200.mgrit import solve
+    from paper_1805_06688_b200.stepper import ProblemSpec
+
+    out = {}
+    ok = True
+    # (1) the same solver on the config's grid and physics at the full run's step sizes, vs the reference's run
+    regimes = {"cfg3": ("cfg3_split.npz", "c3p", dict(Nt=1024, T=1.0 / 16)),
+               "cfg2": ("cfg2_split.npz", "c2p", dict(Nt=512, T=0.125))}
+    if case.name in regimes:
+        fixture, tag, kw = regimes[case.name]
+        g = np.load(os.path.join(REPO, "tests", "golden", fixture))
+        c2 = make_case(case.name, **kw)
+        o2 = type(opts)(**{**opts.__dict__, "max_levels": c2.max_levels})
+        U, tr = solve(ProblemSpec(**c2.problem_kwargs()), o2, device_result=True)
+        keep = [int(k) for k in g[f"{tag}_keep"]]
+        Uk = U[keep].cpu().numpy()
+        R = g[f"{tag}_U"]
+        err = max(float(np.linalg.norm(Uk[i] - R[i]) / max(np.linalg.norm(R[i]), 1e-300)) for i in range(len(keep)))
+        norms = U.norm(dim=1).cpu().numpy()
+        nerr = float(np.max(np.abs(norms - g[f"{tag}_norms"]) / np.maximum(g[f"{tag}_norms"], 1e-300)))
+        same_its = tr.iterations == len(g[f"{tag}_res"]) - 1
+        same_solves = list(tr.spatial_solves) == [int(x) for x in g[f"{tag}_solves"]]
+        good = same_its and same_solves and err <= 1e-10 and nerr <= 1e-10
+        ok &= good
+        out["reference_run"] = {"fixture": f"tests/golden/{fixture}", "case": f"{case.name} Nt={kw['Nt']} T={kw['T']:g}",
+                                "iterations": tr.iterations, "same_iterations": same_its,
+                                "same_spatial_solves": same_solves, "max_rel_l2_kept_points": err,
+                                "max_rel_norm_all_points": nerr, "ok": good}
+    # (2) the timed solve's trace vs the reference algorithm (unpreconditioned CG) run of the full config
+    counts = reference_counts(case)
+    if counts is not None and "residual_norms" in counts and case.tmesh.n_intervals == counts.get("nt"):
+        res = np.array(trace.residual_norms)
+        ref = np.array(counts["residual_norms"])
+        same_its = trace.iterations == counts["mgrit_iterations"]
+        same_solves = list(trace.spatial_solves) == counts["spatial_solves"]
+        hist = bool(res.shape == ref.shape and np.all(np.abs(res - ref) <= 1e-6 * ref + 0.2 * case.halt_tol))
+        good = same_its and same_solves and hist
+        ok &= good
+        out["full_config_trace"] = {"against": f"profiles/{case.name}_reference_counts.json (reference algorithm)",
+                                    "same_iterations": same_its, "same_spatial_solves": same_solves,
+                                    "residual_history_match": hist, "ok": good}
+    out["parity_checked"] = bool(out) and ok
+    return out
 
 
 def run_ours(args):
     import torch
 
     from paper_1805_06688_b200.engine import Engine
+    from paper_1805_06688_b200.flops import fmv_fft, fpc_fft
     from paper_1805_06688_b200.mgrit import solve
     from paper_1805_06688_b200.stepper import ProblemSpec
 
@@ -306,6 +378,8 @@ def run_ours(args):
         barrier()
     launches = eng.launches - launches0
     ms = e0.elapsed_time(e1) / args.steps
+    timed_trace = tr
+    U = None
     # one more (untimed) solve with per-launch CUDA events and counter snapshots: the chain kernel's
     # share of the step and its algorithmic FLOPs (roofline)
     eng.start_trace()
@@ -316,26 +390,49 @@ def run_ours(args):
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = work / (ms * 1e-3)  # whole job: one cfg2 problem, time axis sharded over the ranks
+    value = work / (ms * 1e-3)  # whole job: one problem, time axis sharded over the ranks
 
     # dominant kernel: the chain kernel (all rm_sweep_run launches)
     k_ms = sum(a.elapsed_time(b) for _, a, b, *_ in trace)
     mvs = sum(int((after - before)[2].item()) for _, _, _, before, after, _ in trace)
     pcs = sum(int((after - before)[3].item()) for _, _, _, before, after, _ in trace)
     mvs16 = sum(int((after - before)[4].item()) for _, _, _, before, after, _ in trace)
-    # Algorithmic FLOPs: F_mv per operator apply -- whether it ran on FP64 DMMA or as a
-    # split-FP16 product inside the PCG iteration -- and F_pc per tau application.  The roofline is the
-    # FP64 tensor peak (the arithmetic the path is specified in); the chain kernel executes part of that
-    # work on FP16 tensor cores, which the auxiliary "executed" fields account for separately: its
-    # executed-FLOP time bound is F64/P64 + F16/P16 (mixed_bound_frac = bound / measured time).
     nx_, ny_ = case.grid.nx, case.grid.ny
-    alg = (mvs + mvs16) * fmv(nx_, ny_, eng.flags) + pcs * fpc(nx_, ny_)
-    achieved = alg / (k_ms * 1e-3) / 1e12
-    lp = args.precond in ("tau", "tau16") and nx_ == ny_  # FP16 DST stages: square grids
-    f64 = mvs * fmv(nx_, ny_, eng.flags) + (0.0 if lp else pcs * fpc(nx_, ny_))
-    f16 = (pcs * fpc_dense(nx_, ny_) if lp else 0.0) + mvs16 * fmv_split16(nx_, ny_)
-    t_bound = f64 / (peak * 1e12) + f16 / (FP16_MMA_SYNC_PEAK_TFLOPS * 1e12)
-    traffic, traffic_launch = ncu_traffic()
+    if eng.fft:
+        # FFT chain kernel (csrc/rm_fft.cu): every FLOP is FP64 on the CUDA-core FP64 pipe (no tensor cores);
+        # algorithmic FLOPs = FFTs at 5 L log2 L + symbol combination + scaling per apply / tau application
+        fa, fp = fmv_fft(nx_, ny_), fpc_fft(nx_, ny_)
+        alg = mvs * fa + pcs * fp
+        achieved = alg / (k_ms * 1e-3) / 1e12
+        summ = ncu_summary(True)
+        roof = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": summ.get("dram_bytes_per_launch"),
+                "kernel": "chain_fft_kernel (FP64 tau-PCG chains: block-Toeplitz applies and DST-I stages as "
+                          "512-point FFTs, 8 CTAs per chain)",
+                "achieved_counts": "algorithmic FP64 FLOPs: flops.fmv_fft per operator apply (%.3g), "
+                                   "flops.fpc_fft per tau application (%.3g)" % (fa, fp),
+                "peak_source": "FP64 peak: cuBLAS DGEMM 8192^3 measured in this run (DFMA microbenchmark within 1 %, "
+                               "tools/fp64_peak.cu); FP64 is not in MEASURED_PEAKS.json",
+                "applies_per_step": mvs, "precond_applies_per_step": pcs, "kernel_ms_per_step": k_ms,
+                "kernel_share_of_step": k_ms / ms,
+                "algorithmic_bytes_per_launch": summ.get("algorithmic_bytes_per_launch"),
+                "traffic_launch": summ.get("launch"), "ncu_fp64_pipe_active": summ.get("fp64_pipe_active_pct")}
+    else:
+        # dense DMMA / split-FP16 chain kernels: frac = executed-work bound (F64 at the DGEMM peak plus F16 at
+        # the legacy-MMA peak) over the measured time; the FP64-equivalent figure is auxiliary
+        lp = args.precond in ("tau", "tau16") and nx_ == ny_
+        f64 = mvs * fmv(nx_, ny_, eng.flags) + (0.0 if lp else pcs * fpc(nx_, ny_))
+        f16 = (pcs * fpc_dense(nx_, ny_) if lp else 0.0) + mvs16 * fmv_split16(nx_, ny_)
+        t_bound = f64 / (peak * 1e12) + f16 / (FP16_MMA_SYNC_PEAK_TFLOPS * 1e12)
+        frac = t_bound / (k_ms * 1e-3)
+        alg = (mvs + mvs16) * fmv(nx_, ny_, eng.flags) + pcs * fpc(nx_, ny_)
+        summ = ncu_summary(False)
+        roof = {"bound": "tensor", "achieved": frac * peak, "peak": peak, "unit": "TFLOP/s (FP64-peak equivalent of "
+                "the executed-work bound)", "frac": frac, "traffic": summ.get("dram_bytes_per_launch"),
+                "kernel": "chain_kernel / chain_big_kernel (dense DMMA applies, FP16 DST stages)",
+                "executed_fp64_flops_per_step": f64, "executed_fp16_flops_per_step": f16,
+                "fp16_peak": FP16_MMA_SYNC_PEAK_TFLOPS,
+                "fp64_equivalent_frac": alg / (k_ms * 1e-3) / 1e12 / peak, "kernel_ms_per_step": k_ms}
 
     # end to end through the public API (host inputs, host result)
     # (one untimed call first: the public API's engine cache and the page-locked result block are
@@ -343,13 +440,14 @@ def run_ours(args):
     # solves would)
     e2e_ms = []
     Uh, tr_h = solve(spec, opts)
-    for _ in range(args.steps):
+    for _ in range(max(1, min(args.steps, args.e2e_steps))):
         Uh = None
         barrier()
         t0 = time.perf_counter()
         Uh, tr_h = solve(spec, opts)
         torch.cuda.synchronize()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    Uh = None
     e2e = statistics.median(e2e_ms)
     if dist is not None:
         t = torch.tensor([e2e], device="cuda")
@@ -360,6 +458,7 @@ def run_ours(args):
     h2d = 8 * (2 * ndof + 2 * (N + 1) + 8 * (case.grid.nx + case.grid.ny))
     d2h = 8 * ((N + 1) * ndof + nlev * (N + 1))
 
+    parity = parity_checks(case, opts, timed_trace) if ws == 1 else {"parity_checked": None}
     if rank == 0:
         cpu = None
         counts = reference_counts(case)
@@ -376,28 +475,11 @@ def run_ours(args):
                            parallelism=(f"time slabs x{ws} (contiguous coarse intervals per rank, NCCL C-point "
                                         f"exchange, pipelined coarsest level)" if ws > 1 else "single GPU")),
             "e2e": {"value": work / (e2e * 1e-3), "unit": UNIT,
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": len(e2e_ms)},
             "gpu_launches": launches // args.steps,
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "chain_kernel (fused PCG: FP64 DMMA block-Toeplitz applies for right-hand "
-                                   "sides and true residuals, split-FP16 HMMA applies inside the iteration, tau "
-                                   "DST stages on FP16 HMMA)",
-                         "achieved_counts": "algorithmic FP64-equivalent FLOPs: F_mv per operator apply (FP64 or "
-                                            "split-FP16), F_pc per tau application (flops.py)",
-                         "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (FP64 is not in "
-                                        "MEASURED_PEAKS.json)",
-                         "executed_fp64_flops_per_step": f64, "executed_fp16_flops_per_step": f16,
-                         "fp16_peak": FP16_MMA_SYNC_PEAK_TFLOPS,
-                         "fp16_peak_source": "legacy mma.sync FP16 (tools/lowp_peak.cu, profiles/r01_lowp_peak.txt)",
-                         "mixed_bound_frac": t_bound / (k_ms * 1e-3),
-                         "traffic_launch": traffic_launch,
-                         "flops_per_apply": fmv(case.grid.nx, case.grid.ny, eng.flags), "fp64_applies_per_step": mvs,
-                         "flops_per_precond": fpc(case.grid.nx, case.grid.ny),
-                         "precond_applies_per_step": pcs,
-                         "split_fp16_applies_per_step": mvs16,
-                         "executed_flops_per_split_fp16_apply": fmv_split16(case.grid.nx, case.grid.ny),
-                         "kernel_ms_per_step": k_ms},
+            "roofline": roof,
+            "parity_checked": parity.get("parity_checked"),
+            "parity": parity,
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,
         }
@@ -412,12 +494,13 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--scaling", choices=["weak", "strong"], default="strong",
-                    help="N > 1: strong = the cfg2 problem split over the GPUs (default); weak = one cfg2-sized "
-                         "slab of 4096 fine steps per GPU over a horizon T = N (a different, harder problem)")
+                    help="N > 1: strong = the BASELINE problem split over the GPUs (default); weak = Nt fine steps "
+                         "per GPU over a horizon T = N (a different, harder problem)")
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--config", default="cfg3")
+    ap.add_argument("--e2e-steps", type=int, default=3, help="end-to-end public-API repetitions (median)")
     ap.add_argument("--nt", type=int, default=None)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")

@@ -198,7 +198,9 @@ RM_API int rm_fail_reset(rm_grid* grid, void* stream);
  * Execution flags chosen for a grid (no reference counterpart; informational):
  * bit 0 / bit 1 = the off-diagonal x / y Toeplitz segments of the matvec run merged
  * (T2 first column == first row shifted by one, as for the Riesz stiffness, assembly.py:239-249),
- * which cuts the matvec from 12 n^3 to 8 n^3 FLOPs.  Returns the flags, or -1 for a null grid.
+ * which cuts the matvec from 12 n^3 to 8 n^3 FLOPs; bit 2 = sweeps run the FFT chain kernel (255^2 grids:
+ * operator applies and tau-preconditioner DSTs by 512-point FP64 FFTs; RM_NO_FFT=1 selects the dense DMMA
+ * kernel instead).  Returns the flags, or -1 for a null grid.
  */
 RM_API int rm_grid_flags(const rm_grid* grid);
 

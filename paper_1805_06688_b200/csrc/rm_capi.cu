@@ -237,7 +237,11 @@ int rm_grid_destroy(rm_grid* g) {
   return RM_OK;
 }
 
-int rm_grid_flags(const rm_grid* g) { return g ? g->merge : -1; }
+int rm_grid_flags(const rm_grid* g) {
+  if (!g) return -1;
+  const bool fft = g->fft_ok && !(getenv("RM_NO_FFT") && atoi(getenv("RM_NO_FFT")));
+  return g->merge | (fft ? 4 : 0);
+}
 
 int rm_apply_batched(const rm_grid* g, int which, int batch, const double* d_dt, int sign, const double* d_v,
                      int64_t v_stride, double* d_out, int64_t out_stride, void* stream) {

@@ -111,9 +111,15 @@ class Engine:
         _native.check(self.lib.rm_grid_create(self.nx, self.ny, *ptrs, gens.sx, gens.sy, self.kx, self.ky,
                                               gens.mass_scale, C.byref(handle)), "rm_grid_create")
         self.handle = handle
-        self.flags = int(self.lib.rm_grid_flags(handle))  # bit 0/1: merged off-diagonal x/y matvec segments
+        # bit 0/1: merged off-diagonal x/y matvec segments; bit 2: sweeps run the FFT kernel (rm_fft.cu)
+        self.flags = int(self.lib.rm_grid_flags(handle))
         self.launches = 0
         self.trace = None  # list of (tag, start event, end event, counters-before) when profiling
+
+    @property
+    def fft(self) -> bool:
+        """Sweeps of this grid run the FFT chain kernel (FP64 FFT applies and DSTs)."""
+        return bool(self.flags & 4)
 
     def start_trace(self):
         self.trace = []

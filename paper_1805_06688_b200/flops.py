@@ -36,5 +36,29 @@ def fmv_split16(nx: int, ny: int) -> float:
     return 3.0 * (3 * 2.0 * nx * nx * ny + 3 * 2.0 * ny * ny * nx)
 
 
+def fft_flops(L: int) -> float:
+    """One complex FFT of length L (conventional 5 L log2 L)."""
+    import math
+
+    return 5.0 * L * math.log2(L)
+
+
+def fmv_fft(nx: int, ny: int) -> float:
+    """One operator apply by the FFT kernel (csrc/rm_fft.cu), algorithmic: per direction, the rows (columns)
+    as ceil(n/2) packed complex pairs, a forward and an inverse L-point FFT each (L = 2(n+1)), the three-term
+    symbol combination (3 complex multiplies + 2 adds per point), plus the final scale-and-add."""
+    L = 2 * (max(nx, ny) + 1)
+    px, py = (ny + 1) // 2, (nx + 1) // 2
+    per_pair = 2.0 * fft_flops(L) + 22.0 * L
+    return (px + py) * per_pair + 2.0 * nx * ny
+
+
+def fpc_fft(nx: int, ny: int) -> float:
+    """One tau-preconditioner application by the FFT kernel: four DST-I passes (one odd-extended L-point FFT
+    per packed pair) and the diagonal scaling."""
+    L = 2 * (max(nx, ny) + 1)
+    return 2.0 * ((ny + 1) // 2 + (nx + 1) // 2) * fft_flops(L) + 2.0 * nx * ny
+
+
 # legacy mma.sync m16n8k16 FP16 -> FP32 on B200, measured with tools/lowp_peak.cu (profiles/r01_lowp_peak.txt)
 FP16_MMA_SYNC_PEAK_TFLOPS = 555.0

@@ -79,6 +79,11 @@ def test_benched_regime_matches_reference(golden, fixture, tag, name, nt, T, pre
     # dominated by the inner solves' own 1e-12 tolerance noise (~1e-9 here), which differs between any two
     # correct inner solvers (the reference's plain CG and tau-PCG), so there it agrees to 0.2 halt_tol
     np.testing.assert_allclose(trace.residual_norms, ref_res, rtol=1e-6, atol=0.2 * case.halt_tol)
+    if pre == "none":
+        # the reference's own (unpreconditioned) CG: the same inner work, which pins the reference-equivalent
+        # counts bench.py's CPU extrapolation uses (profiles/<config>_reference_counts.json)
+        cg_ref = g[f"{tag}_cgits"]
+        assert abs(trace.cg_iterations[-1] - cg_ref[-1]) <= 0.01 * cg_ref[-1] + 2, (trace.cg_iterations, cg_ref)
     if pre == "tau" and name == "cfg2":
         # the regime exists to exercise the split-FP16 in-iteration applies of the default path
         assert counters(hier[0])[4] > 0
