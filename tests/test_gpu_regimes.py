@@ -104,3 +104,20 @@ def test_cfg4_divergence_matches_reference(golden):
     assert np.array_equal(np.array(trace.spatial_solves), g["c4d_solves"])
     assert np.all(np.diff(trace.residual_norms) > 0)  # grows every cycle, as in the reference
     check_points(U, g, "c4d")
+
+
+@pytest.mark.parametrize("pre", ["tau", "none"])
+def test_cfg4_full_graded_grid_matches_reference(golden, pre):
+    """cfg4's physics on its full graded time grid (Nt = 8192, t_n = (n/Nt)^2: every fine dt of the BASELINE run,
+    levels 8192/1024/128/16/2) at a reduced 63^2 grid, where MGRIT converges: time-dependent propagators at
+    every step, parity with the reference's own run."""
+    g = golden("cfg4_fullnt.npz")
+    case = make_case("cfg4", M=64)
+    opts = MgritOptions(m=case.m, max_levels=case.max_levels, halt_tol=case.halt_tol, cg_rel_tol=case.cg_rel_tol,
+                        cg_preconditioner=pre)
+    U, trace = solve(ProblemSpec(**case.problem_kwargs()), opts)
+    assert trace.converged
+    assert trace.iterations == int(g["c4n_its"])
+    assert np.array_equal(np.array(trace.spatial_solves), g["c4n_solves"])
+    check_points(U, g, "c4n")
+    np.testing.assert_allclose(trace.residual_norms, g["c4n_res"], rtol=1e-6, atol=0.2 * case.halt_tol)
