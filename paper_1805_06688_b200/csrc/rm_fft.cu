@@ -54,54 +54,80 @@ constexpr int TS = 34;                // transpose row stride (conflict-free 16-
 constexpr int NVEC = 6;               // per-chain vectors
 constexpr size_t VEC = (size_t)NP * NP;
 constexpr size_t DIV = (size_t)H * 16 * 32 * 2;  // per-CTA 1/d(s) cache (doubles)
-constexpr size_t SMEM = sizeof(double2) * ((size_t)NSLOT * SLOT + L + 16 + 6 * L) + sizeof(double) * (4 * 32) + 64;
+constexpr int SLOTF = 1089;            // float2 per slot in the FP32 (preconditioner) passes: odd -> conflict-free
+static_assert(SLOTF * 8 <= SLOT * 16, "FP32 slots overlay the FP64 ones");
+constexpr size_t SMEM = sizeof(double2) * ((size_t)NSLOT * SLOT + L + 16 + 6 * L) + sizeof(double) * (4 * 32) +
+                        sizeof(float2) * (L + 16) + 64;
 static_assert(SMEM <= 227 * 1024, "shared memory budget");
 
-__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+// complex arithmetic on double2 / float2 (the preconditioner's DSTs run in FP32, see precond)
+template <class V>
+struct Cx;
+template <>
+struct Cx<double2> {
+  using R = double;
+  static __device__ __forceinline__ double2 mk(double x, double y) { return make_double2(x, y); }
+  static __device__ __forceinline__ double ffma(double a, double b, double c) { return fma(a, b, c); }
+};
+template <>
+struct Cx<float2> {
+  using R = float;
+  static __device__ __forceinline__ float2 mk(float x, float y) { return make_float2(x, y); }
+  static __device__ __forceinline__ float ffma(float a, float b, float c) { return fmaf(a, b, c); }
+};
+
+template <class V>
+__device__ __forceinline__ V cadd(V a, V b) { return Cx<V>::mk(a.x + b.x, a.y + b.y); }
+template <class V>
+__device__ __forceinline__ V csub(V a, V b) { return Cx<V>::mk(a.x - b.x, a.y - b.y); }
+template <class V>
+__device__ __forceinline__ V cmul(V a, V b) {
+  return Cx<V>::mk(Cx<V>::ffma(a.x, b.x, -a.y * b.y), Cx<V>::ffma(a.x, b.y, a.y * b.x));
 }
-__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {  // a * conj(b)
-  return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
+template <class V>
+__device__ __forceinline__ V cmulc(V a, V b) {  // a * conj(b)
+  return Cx<V>::mk(Cx<V>::ffma(a.x, b.x, a.y * b.y), Cx<V>::ffma(a.y, b.x, -a.x * b.y));
 }
-__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
-__device__ __forceinline__ double2 shfl_xor2(double2 a, int m) {
-  return make_double2(__shfl_xor_sync(0xffffffffu, a.x, m), __shfl_xor_sync(0xffffffffu, a.y, m));
+template <class V>
+__device__ __forceinline__ V cscale(V a, typename Cx<V>::R s) { return Cx<V>::mk(a.x * s, a.y * s); }
+template <class V>
+__device__ __forceinline__ V shfl_xor2(V a, int m) {
+  return Cx<V>::mk(__shfl_xor_sync(0xffffffffu, a.x, m), __shfl_xor_sync(0xffffffffu, a.y, m));
 }
 
 // DFT of length 4: forward kernel W4 = -i, inverse +i
-template <bool INV>
-__device__ __forceinline__ void dft4(double2& a0, double2& a1, double2& a2, double2& a3) {
-  const double2 s02 = cadd(a0, a2), d02 = csub(a0, a2), s13 = cadd(a1, a3), d13 = csub(a1, a3);
+template <bool INV, class V>
+__device__ __forceinline__ void dft4(V& a0, V& a1, V& a2, V& a3) {
+  const V s02 = cadd(a0, a2), d02 = csub(a0, a2), s13 = cadd(a1, a3), d13 = csub(a1, a3);
   a0 = cadd(s02, s13);
   a2 = csub(s02, s13);
   if (!INV) {
-    a1 = make_double2(d02.x + d13.y, d02.y - d13.x);
-    a3 = make_double2(d02.x - d13.y, d02.y + d13.x);
+    a1 = Cx<V>::mk(d02.x + d13.y, d02.y - d13.x);
+    a3 = Cx<V>::mk(d02.x - d13.y, d02.y + d13.x);
   } else {
-    a1 = make_double2(d02.x - d13.y, d02.y + d13.x);
-    a3 = make_double2(d02.x + d13.y, d02.y - d13.x);
+    a1 = Cx<V>::mk(d02.x - d13.y, d02.y + d13.x);
+    a3 = Cx<V>::mk(d02.x + d13.y, d02.y - d13.x);
   }
 }
 
 // y *= W16^{e} (forward) or W16^{-e} (inverse), e in {1, 2, 3, 4, 6, 9}
-template <bool INV, int E>
-__device__ __forceinline__ void tw16(double2& y) {
+template <bool INV, int E, class V>
+__device__ __forceinline__ void tw16(V& y) {
+  using R = typename Cx<V>::R;
   constexpr double C1 = 0.92387953251128674, S1 = 0.38268343236508978, R2 = 0.70710678118654752;
   if constexpr (E == 4) {
-    y = INV ? make_double2(-y.y, y.x) : make_double2(y.y, -y.x);
+    y = INV ? Cx<V>::mk(-y.y, y.x) : Cx<V>::mk(y.y, -y.x);
   } else {
     constexpr double c = E == 1 ? C1 : E == 2 ? R2 : E == 3 ? S1 : E == 6 ? -R2 : -C1;
     constexpr double sn = E == 1 ? S1 : E == 2 ? R2 : E == 3 ? C1 : E == 6 ? R2 : -S1;  // sin(2 pi E / 16)
-    const double2 w = make_double2(c, INV ? sn : -sn);
+    const V w = Cx<V>::mk((R)c, (R)(INV ? sn : -sn));
     y = cmul(y, w);
   }
 }
 
 // in place: a[k] = sum_n a[n] W16^{+-nk}
-template <bool INV>
-__device__ __forceinline__ void dft16(double2 (&a)[16]) {
+template <bool INV, class V>
+__device__ __forceinline__ void dft16(V (&a)[16]) {
   // n = 4 n1 + n2, k = k1 + 4 k2
 #pragma unroll
   for (int n2 = 0; n2 < 4; ++n2) dft4<INV>(a[n2], a[4 + n2], a[8 + n2], a[12 + n2]);
@@ -118,7 +144,7 @@ __device__ __forceinline__ void dft16(double2 (&a)[16]) {
 #pragma unroll
   for (int k1 = 0; k1 < 4; ++k1) dft4<INV>(a[4 * k1], a[4 * k1 + 1], a[4 * k1 + 2], a[4 * k1 + 3]);
   // a[4 k1 + k2] = X[k1 + 4 k2] -> a[k]
-  double2 t[16];
+  V t[16];
 #pragma unroll
   for (int k = 0; k < 16; ++k) t[k] = a[4 * (k & 3) + (k >> 2)];
 #pragma unroll
@@ -126,9 +152,9 @@ __device__ __forceinline__ void dft16(double2 (&a)[16]) {
 }
 
 // forward 512-point FFT of one warp.  in: a[m] = x[lane + 32 m]; out: a[r] = X[q + 16 (r + 16 v)] with
-// q = lane >> 1, v = lane & 1.  `scr` (>= 16 x TS double2) is clobbered.
-__device__ __forceinline__ void fft512_fwd(double2 (&a)[16], double2* scr, const double2* tw2, const double2* tw32,
-                                           int lane) {
+// q = lane >> 1, v = lane & 1.  `scr` (>= 16 x TS elements) is clobbered.
+template <class V>
+__device__ __forceinline__ void fft512_fwd(V (&a)[16], V* scr, const V* tw2, const V* tw32, int lane) {
   dft16<false>(a);
 #pragma unroll
   for (int q = 1; q < 16; ++q) a[q] = cmul(a[q], tw2[q * 32 + lane]);  // W512^{lane q}
@@ -142,21 +168,21 @@ __device__ __forceinline__ void fft512_fwd(double2 (&a)[16], double2* scr, const
   dft16<false>(a);
 #pragma unroll
   for (int r = 0; r < 16; ++r) {
-    const double2 o = shfl_xor2(a[r], 1);
-    const double2 a0 = v ? o : a[r], a1 = v ? a[r] : o;
-    const double2 t = cmul(a1, tw32[r]);
+    const V o = shfl_xor2(a[r], 1);
+    const V a0 = v ? o : a[r], a1 = v ? a[r] : o;
+    const V t = cmul(a1, tw32[r]);
     a[r] = v ? csub(a0, t) : cadd(a0, t);
   }
 }
 
 // unnormalised inverse (x 512) of fft512_fwd: in k-layout, out a[m] = 512 x[lane + 32 m]
-__device__ __forceinline__ void fft512_inv(double2 (&a)[16], double2* scr, const double2* tw2, const double2* tw32,
-                                           int lane) {
+template <class V>
+__device__ __forceinline__ void fft512_inv(V (&a)[16], V* scr, const V* tw2, const V* tw32, int lane) {
   const int q2 = lane >> 1, v = lane & 1;
 #pragma unroll
   for (int r = 0; r < 16; ++r) {
-    const double2 o = shfl_xor2(a[r], 1);
-    const double2 y0 = v ? o : a[r], y1 = v ? a[r] : o;
+    const V o = shfl_xor2(a[r], 1);
+    const V y0 = v ? o : a[r], y1 = v ? a[r] : o;
     a[r] = v ? cmulc(csub(y0, y1), tw32[r]) : cadd(y0, y1);
   }
   dft16<true>(a);
@@ -176,8 +202,10 @@ __device__ __forceinline__ int klay(int lane, int r) { return (lane >> 1) + 16 *
 // orthonormal DST-I (order 255) of a packed pair, forward-FFT form.  in: a[m] = (x_a, x_b)[lane + 32 m],
 // m < 8 (index 255 must be 0); out: k-layout w[k] = ((S x_a)[k-1], (S x_b)[k-1]) for 1 <= k <= 255 (and the
 // odd mirror w[512 - k] = -w[k]).  `slot` is clobbered.
-__device__ __forceinline__ void dst_fwd(double2 (&a)[16], double2* slot, const double2* tw2, const double2* tw32,
-                                        int lane, double half_c) {
+template <class V>
+__device__ __forceinline__ void dst_fwd(V (&a)[16], V* slot, const V* tw2, const V* tw32, int lane,
+                                        typename Cx<V>::R half_c) {
+  using R = typename Cx<V>::R;
   __syncwarp();
 #pragma unroll
   for (int m = 0; m < 8; ++m) slot[lane + 32 * m] = a[m];
@@ -186,22 +214,24 @@ __device__ __forceinline__ void dst_fwd(double2 (&a)[16], double2* slot, const d
   for (int m = 0; m < 16; ++m) {
     const int n = lane + 32 * m;
     if (m < 8) {
-      a[m] = n >= 1 ? slot[n - 1] : make_double2(0.0, 0.0);
+      a[m] = n >= 1 ? slot[n - 1] : Cx<V>::mk(R(0), R(0));
     } else {
-      const double2 t = slot[(511 - n) & 511];
-      a[m] = n >= 257 ? make_double2(-t.x, -t.y) : make_double2(0.0, 0.0);
+      const V t = slot[(511 - n) & 511];
+      a[m] = n >= 257 ? Cx<V>::mk(-t.x, -t.y) : Cx<V>::mk(R(0), R(0));
     }
   }
   fft512_fwd(a, slot, tw2, tw32, lane);
   // (S x)[k-1] = c D[k], X = FFT(ext) = -2 i D  ->  w = (c/2) i X
 #pragma unroll
-  for (int r = 0; r < 16; ++r) a[r] = make_double2(-half_c * a[r].y, half_c * a[r].x);
+  for (int r = 0; r < 16; ++r) a[r] = Cx<V>::mk(-half_c * a[r].y, half_c * a[r].x);
 }
 
 // orthonormal DST-I from k-layout odd-symmetric input w (w[0] = w[256] = 0, w[512-k] = -w[k]), inverse-FFT
 // form.  out: a[m] = ((S w_a), (S w_b))[lane + 32 m], m < 8 (index 255 -> 0).  `slot` is clobbered.
-__device__ __forceinline__ void dst_inv(double2 (&a)[16], double2* slot, const double2* tw2, const double2* tw32,
-                                        int lane, double half_c) {
+template <class V>
+__device__ __forceinline__ void dst_inv(V (&a)[16], V* slot, const V* tw2, const V* tw32, int lane,
+                                        typename Cx<V>::R half_c) {
+  using R = typename Cx<V>::R;
   fft512_inv(a, slot, tw2, tw32, lane);
   // I = sum_k w[k] e^{+2 pi i k n / L} = 2 i D(w)[n]  ->  (S w)[n-1] = c D[n] = (c/2)(-i) I[n]
   __syncwarp();
@@ -211,8 +241,8 @@ __device__ __forceinline__ void dst_inv(double2 (&a)[16], double2* slot, const d
 #pragma unroll
   for (int m = 0; m < 8; ++m) {
     const int i = lane + 32 * m;
-    const double2 t = slot[(i + 1) & 511];
-    a[m] = i + 1 <= 255 ? make_double2(half_c * t.y, -half_c * t.x) : make_double2(0.0, 0.0);
+    const V t = slot[(i + 1) & 511];
+    a[m] = i + 1 <= 255 ? Cx<V>::mk(half_c * t.y, -half_c * t.x) : Cx<V>::mk(R(0), R(0));
   }
 }
 
@@ -293,9 +323,11 @@ struct Ctx {
   __device__ __forceinline__ double* XV() const { return base + 3 * VEC; }  // iterate (owner rows)
   __device__ __forceinline__ double* RV() const { return base + 4 * VEC; }  // residual
   __device__ __forceinline__ double* BV() const { return base + 5 * VEC; }  // right-hand side
-  // this CTA's 1/d(s) of its column pairs, k-layout [warp][r][lane]
-  __device__ __forceinline__ double2* DI() const {
-    return reinterpret_cast<double2*>(base + NVEC * VEC + (size_t)rank * DIV);
+  __device__ __forceinline__ float* SRf() const { return reinterpret_cast<float*>(SR()); }  // FP32 row-DST output
+  __device__ __forceinline__ float* WVf() const { return reinterpret_cast<float*>(WV()); }  // FP32 column-DST output
+  // this CTA's 1/d(s) of its column pairs, k-layout [pair][r][lane]
+  __device__ __forceinline__ float2* DI() const {
+    return reinterpret_cast<float2*>(base + NVEC * VEC + (size_t)rank * DIV);
   }
 };
 
@@ -308,8 +340,13 @@ __device__ __forceinline__ const double2* TW2() { return smem2() + NSLOT * SLOT;
 __device__ __forceinline__ const double2* TW32() { return smem2() + NSLOT * SLOT + L; }
 __device__ __forceinline__ const double2* SYM() { return smem2() + NSLOT * SLOT + L + 16; }
 __device__ __forceinline__ double* WRED() { return reinterpret_cast<double*>(smem2() + NSLOT * SLOT + L + 16 + 6 * L); }
+// FP32 twiddles (tw2f[q * 32 + t] = W512^{q t}, tw32f[r] = W32^r) and the FP32 view of the slots
+__device__ __forceinline__ const float2* TW2F() { return reinterpret_cast<const float2*>(WRED() + 4 * 32); }
+__device__ __forceinline__ const float2* TW32F() { return TW2F() + L; }
+__device__ __forceinline__ float2* SLOTSF() { return reinterpret_cast<float2*>(smem2()); }
 constexpr int NX = NP - 1;  // the kernel serves n = 255 grids only (fft_supported)
 constexpr double HALF_C = 0.044194173824159220;  // sqrt(2 / 256) / 2
+constexpr float HALF_CF = 0.0441941738f;
 
 #define RM_OWN_FOR _Pragma("unroll") for (int p = 0; p < NOWN; ++p) _Pragma("unroll") for (int m = 0; m < 8; ++m)
 
@@ -482,11 +519,11 @@ __device__ __forceinline__ void dinv_refresh(Ctx& c, double s) {
     for (int r = 0; r < 16; ++r) {
       const int k = klay(c.lane(), r);
       const int kk = k <= 256 ? k : 512 - k;
-      double2 w = make_double2(0.0, 0.0);
+      float2 w = make_float2(0.f, 0.f);
       if (kk >= 1 && kk <= 255) {
         const int a = kk - 1;
-        if (ca < NX) w.x = 1.0 / (__ldg(c.P->dmT + ca * NX + a) + s * __ldg(c.P->dkT + ca * NX + a));
-        if (cb < NX) w.y = 1.0 / (__ldg(c.P->dmT + cb * NX + a) + s * __ldg(c.P->dkT + cb * NX + a));
+        if (ca < NX) w.x = (float)(1.0 / (__ldg(c.P->dmT + ca * NX + a) + s * __ldg(c.P->dkT + ca * NX + a)));
+        if (cb < NX) w.y = (float)(1.0 / (__ldg(c.P->dmT + cb * NX + a) + s * __ldg(c.P->dkT + cb * NX + a)));
       }
       c.DI()[(q * 16 + r) * 32 + c.lane()] = w;
     }
@@ -494,18 +531,20 @@ __device__ __forceinline__ void dinv_refresh(Ctx& c, double s) {
 }
 
 // z = P(s)^-1 r = (Sy x Sx) diag(1/d(s)) (Sy x Sx) r for the owner rows (two group barriers)
+// The DST stages run as FP32 FFTs (FP32 intermediates SR / WV, FP32 1/d): P^-1 only steers the iteration --
+// every stop is decided on the FP64 true residual -- and FP32 keeps it within ~1e-7 of the FP64 operator.
 __device__ __forceinline__ void precond(Ctx& c, const double (&r)[NOWN][8], double (&z)[NOWN][8], double s) {
-  double2* slots = SLOTS();
+  float2* slots = SLOTSF();
   dinv_refresh(c, s);
 #pragma unroll 1
   for (int h = 0; h < PPW; ++h) {  // SR[own rows] = Sx r (x-frequency along the row), pairs q = warp + WARPS h
-    double2 a[16];
+    float2 a[16];
 #pragma unroll
-    for (int m = 0; m < 8; ++m) a[m] = make_double2(r[2 * h][m], r[2 * h + 1][m]);
-    dst_fwd(a, slots + (c.warp() + WARPS * h) * SLOT, TW2(), TW32(), c.lane(), HALF_C);
+    for (int m = 0; m < 8; ++m) a[m] = make_float2((float)r[2 * h][m], (float)r[2 * h + 1][m]);
+    dst_fwd(a, slots + (c.warp() + WARPS * h) * SLOTF, TW2F(), TW32F(), c.lane(), HALF_CF);
     if ((c.lane() & 1) == 0) {
-      double* sa = c.SR() + own_j(c, 2 * h) * NP - 1;
-      double* sb = c.SR() + own_j(c, 2 * h + 1) * NP - 1;
+      float* sa = c.SRf() + own_j(c, 2 * h) * NP - 1;
+      float* sb = c.SRf() + own_j(c, 2 * h + 1) * NP - 1;
 #pragma unroll
       for (int rr = 0; rr < 16; ++rr) {
         const int k = klay(c.lane(), rr);
@@ -520,25 +559,25 @@ __device__ __forceinline__ void precond(Ctx& c, const double (&r)[NOWN][8], doub
   {  // column pass: WV[:, own columns] = Sy diag(1/d) Sy SR
     for (int idx = c.tid(); idx < NP * H; idx += THREADS) {
       const int j = idx / H, q = idx % H;
-      const double* row = c.SR() + j * NP + c.C0();
-      slots[(q + 1) * SLOT + j] = make_double2(__ldcg(row + q), __ldcg(row + q + H));
+      const float* row = c.SRf() + j * NP + c.C0();
+      slots[(q + 1) * SLOTF + j] = make_float2(__ldcg(row + q), __ldcg(row + q + H));
     }
     __syncthreads();
 #pragma unroll 1
     for (int h = 0; h < PPW; ++h) {
       const int q = c.warp() + WARPS * h;
-      double2* sl = slots + (q + 1) * SLOT;
-      double2 a[16];
+      float2* sl = slots + (q + 1) * SLOTF;
+      float2 a[16];
 #pragma unroll
       for (int m = 0; m < 8; ++m) a[m] = sl[c.lane() + 32 * m];
-      dst_fwd(a, sl, TW2(), TW32(), c.lane(), HALF_C);
-      const double2* di = c.DI() + q * 16 * 32 + c.lane();
+      dst_fwd(a, sl, TW2F(), TW32F(), c.lane(), HALF_CF);
+      const float2* di = c.DI() + q * 16 * 32 + c.lane();
 #pragma unroll
       for (int rr = 0; rr < 16; ++rr) {
-        const double2 d = __ldcg(di + rr * 32);
-        a[rr] = make_double2(a[rr].x * d.x, a[rr].y * d.y);
+        const float2 d = __ldcg(di + rr * 32);
+        a[rr] = make_float2(a[rr].x * d.x, a[rr].y * d.y);
       }
-      dst_inv(a, sl, TW2(), TW32(), c.lane(), HALF_C);
+      dst_inv(a, sl, TW2F(), TW32F(), c.lane(), HALF_CF);
       __syncwarp();
 #pragma unroll
       for (int m = 0; m < 8; ++m) sl[c.lane() + 32 * m] = a[m];
@@ -546,32 +585,32 @@ __device__ __forceinline__ void precond(Ctx& c, const double (&r)[NOWN][8], doub
     __syncthreads();
     for (int idx = c.tid(); idx < NP * H; idx += THREADS) {
       const int j = idx / H, q = idx % H;
-      const double2 t = slots[(q + 1) * SLOT + j];
-      c.WV()[j * NP + c.C0() + q] = t.x;
-      c.WV()[j * NP + c.C0() + q + H] = t.y;
+      const float2 t = slots[(q + 1) * SLOTF + j];
+      c.WVf()[j * NP + c.C0() + q] = t.x;
+      c.WVf()[j * NP + c.C0() + q + H] = t.y;
     }
   }
   gsync(c.sy);
 #pragma unroll 1
   for (int h = 0; h < PPW; ++h) {  // z[own rows] = Sx WV[own rows]
-    double2 a[16];
-    const double* wa = c.WV() + own_j(c, 2 * h) * NP;
-    const double* wb = c.WV() + own_j(c, 2 * h + 1) * NP;
+    float2 a[16];
+    const float* wa = c.WVf() + own_j(c, 2 * h) * NP;
+    const float* wb = c.WVf() + own_j(c, 2 * h + 1) * NP;
 #pragma unroll
     for (int rr = 0; rr < 16; ++rr) {
       const int k = klay(c.lane(), rr);
-      double2 w = make_double2(0.0, 0.0);
+      float2 w = make_float2(0.f, 0.f);
       if (k >= 1 && k <= 255)
-        w = make_double2(__ldcg(wa + k - 1), __ldcg(wb + k - 1));
+        w = make_float2(__ldcg(wa + k - 1), __ldcg(wb + k - 1));
       else if (k >= 257)
-        w = make_double2(-__ldcg(wa + 511 - k), -__ldcg(wb + 511 - k));
+        w = make_float2(-__ldcg(wa + 511 - k), -__ldcg(wb + 511 - k));
       a[rr] = w;
     }
-    dst_inv(a, slots + (c.warp() + WARPS * h) * SLOT, TW2(), TW32(), c.lane(), HALF_C);
+    dst_inv(a, slots + (c.warp() + WARPS * h) * SLOTF, TW2F(), TW32F(), c.lane(), HALF_CF);
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
-      z[2 * h][m] = own_valid(c, 2 * h, m) ? a[m].x : 0.0;
-      z[2 * h + 1][m] = own_valid(c, 2 * h + 1, m) ? a[m].y : 0.0;
+      z[2 * h][m] = own_valid(c, 2 * h, m) ? (double)a[m].x : 0.0;
+      z[2 * h + 1][m] = own_valid(c, 2 * h + 1, m) ? (double)a[m].y : 0.0;
     }
   }
 }
@@ -628,11 +667,13 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
       double sn, cs;
       sincospi(-2.0 * (double)(q * t) / (double)L, &sn, &cs);
       tw2[i] = make_double2(cs, sn);
+      const_cast<float2*>(TW2F())[i] = make_float2((float)cs, (float)sn);
     }
     if (tid < 16) {
       double sn, cs;
       sincospi(-2.0 * (double)(16 * tid) / (double)L, &sn, &cs);
       tw32[tid] = make_double2(cs, sn);
+      const_cast<float2*>(TW32F())[tid] = make_float2((float)cs, (float)sn);
     }
     for (int i = tid; i < 6 * L; i += THREADS) sym[i] = P.fsym[i];
   }

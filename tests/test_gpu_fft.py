@@ -56,7 +56,8 @@ def test_fft_precond_matches_numpy():
                     for v, dt in zip(V, dts)])
     got = eng.precond_apply(torch.from_numpy(V).cuda(), torch.from_numpy(dts).cuda(), "tau64").cpu().numpy()
     for k in range(3):
-        assert rel(got[k], ref[k]) <= 1e-12, (k, rel(got[k], ref[k]))
+        # the DST stages run as FP32 FFTs (the preconditioner only steers the FP64-checked iteration)
+        assert rel(got[k], ref[k]) <= 2e-6, (k, rel(got[k], ref[k]))
 
 
 @pytest.mark.parametrize("pre", ["none", "tau"])
