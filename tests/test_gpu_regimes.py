@@ -121,3 +121,22 @@ def test_cfg4_full_graded_grid_matches_reference(golden, pre):
     assert np.array_equal(np.array(trace.spatial_solves), g["c4n_solves"])
     check_points(U, g, "c4n")
     np.testing.assert_allclose(trace.residual_norms, g["c4n_res"], rtol=1e-6, atol=0.2 * case.halt_tol)
+
+
+@pytest.mark.parametrize("pre", ["tau", "none"])
+def test_cfg2_full_matches_reference(golden, pre):
+    """BASELINE configs[1] at full size (127^2 x 4096, multilevel m = 8) against the reference's own full run
+    (6,668 s on 4 CPU threads): iteration count, spatial solves, CG totals (reference algorithm), points."""
+    g = golden("cfg2_full.npz")
+    case = make_case("cfg2")
+    opts = MgritOptions(m=case.m, max_levels=case.max_levels, halt_tol=case.halt_tol, cg_rel_tol=case.cg_rel_tol,
+                        cg_preconditioner=pre)
+    U, trace = solve(ProblemSpec(**case.problem_kwargs()), opts)
+    assert trace.converged
+    assert trace.iterations == int(g["c2f_its"]) == 21
+    assert np.array_equal(np.array(trace.spatial_solves), g["c2f_solves"])
+    if pre == "none":
+        cg_ref = g["c2f_cgits"]
+        assert abs(trace.cg_iterations[-1] - cg_ref[-1]) <= 0.01 * cg_ref[-1], (trace.cg_iterations[-1], cg_ref[-1])
+    check_points(U, g, "c2f")
+    np.testing.assert_allclose(trace.residual_norms, g["c2f_res"], rtol=1e-6, atol=0.2 * case.halt_tol)
