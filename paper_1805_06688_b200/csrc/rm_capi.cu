@@ -69,7 +69,7 @@ struct rm_grid {
   // FFT kernel (rm_fft.cu): 255^2 grids
   bool fft_ok = false;
   int fft_slots = 0;
-  double2* d_fsym = nullptr;
+  double* d_fsym = nullptr;
   double* d_fscratch = nullptr;
   double* d_dmT = nullptr;
   double* d_dkT = nullptr;
@@ -144,8 +144,8 @@ int rm_grid_create(int nx, int ny, const double* t1x_col, const double* t1x_row,
   if (const char* m = getenv("RM_MERGE")) g->merge &= atoi(m);
   std::vector<double> fsym;
   if (rm::fft_supported(np, nx, ny)) {
-    fsym.resize(2 * 6 * 512);
-    rm::fft_symbols(tab.data(), np, GL, fsym.data());
+    fsym.resize(6 * 512);
+    if (!rm::fft_symbols(tab.data(), np, GL, fsym.data())) fsym.clear();  // generators without the symmetries
   }
   cudaError_t e;
   int maxc = 1;

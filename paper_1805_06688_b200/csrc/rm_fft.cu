@@ -56,7 +56,7 @@ constexpr size_t VEC = (size_t)NP * NP;
 constexpr size_t DIV = (size_t)H * 16 * 32 * 2;  // per-CTA 1/d(s) cache (doubles)
 constexpr int SLOTF = 1089;            // float2 per slot in the FP32 (preconditioner) passes: odd -> conflict-free
 static_assert(SLOTF * 8 <= SLOT * 16, "FP32 slots overlay the FP64 ones");
-constexpr size_t SMEM = sizeof(double2) * ((size_t)NSLOT * SLOT + L + 16 + 6 * L) + sizeof(double) * (4 * 32) +
+constexpr size_t SMEM = sizeof(double2) * ((size_t)NSLOT * SLOT + L + 16 + 3 * L) + sizeof(double) * (4 * 32) +
                         sizeof(float2) * (L + 16) + 64;
 static_assert(SMEM <= 227 * 1024, "shared memory budget");
 
@@ -151,13 +151,30 @@ __device__ __forceinline__ void dft16(V (&a)[16]) {
   for (int k = 0; k < 16; ++k) a[k] = t[k];
 }
 
+// stage-1 twiddles W512^{lane q}, q = 1..15, from six table entries (q = a + 4 b: W^{lane a} W^{4 lane b});
+// CONJ: their conjugates (inverse transform)
+template <bool CONJ, class V>
+__device__ __forceinline__ void twiddle_stage1(V (&a)[16], const V* tw2, int lane) {
+  V wa[4], wb[4];
+#pragma unroll
+  for (int k = 1; k < 4; ++k) {
+    wa[k] = tw2[k * 32 + lane];
+    wb[k] = tw2[4 * k * 32 + lane];
+  }
+#pragma unroll
+  for (int q = 1; q < 16; ++q) {
+    const int qa = q & 3, qb = q >> 2;
+    const V w = qa == 0 ? wb[qb] : (qb == 0 ? wa[qa] : cmul(wa[qa], wb[qb]));
+    a[q] = CONJ ? cmulc(a[q], w) : cmul(a[q], w);
+  }
+}
+
 // forward 512-point FFT of one warp.  in: a[m] = x[lane + 32 m]; out: a[r] = X[q + 16 (r + 16 v)] with
 // q = lane >> 1, v = lane & 1.  `scr` (>= 16 x TS elements) is clobbered.
 template <class V>
 __device__ __forceinline__ void fft512_fwd(V (&a)[16], V* scr, const V* tw2, const V* tw32, int lane) {
   dft16<false>(a);
-#pragma unroll
-  for (int q = 1; q < 16; ++q) a[q] = cmul(a[q], tw2[q * 32 + lane]);  // W512^{lane q}
+  twiddle_stage1<false>(a, tw2, lane);  // W512^{lane q}
   __syncwarp();
 #pragma unroll
   for (int q = 0; q < 16; ++q) scr[q * TS + lane] = a[q];
@@ -192,8 +209,7 @@ __device__ __forceinline__ void fft512_inv(V (&a)[16], V* scr, const V* tw2, con
   __syncwarp();
 #pragma unroll
   for (int q = 0; q < 16; ++q) a[q] = scr[q * TS + lane];
-#pragma unroll
-  for (int q = 1; q < 16; ++q) a[q] = cmulc(a[q], tw2[q * 32 + lane]);
+  twiddle_stage1<true>(a, tw2, lane);
   dft16<true>(a);
 }
 
@@ -305,7 +321,24 @@ __device__ __forceinline__ void greduce(double (&part)[NV], double* wred, Sync& 
 
 // ---- per-CTA context and the kernel's building blocks (all force-inlined: the owner vectors stay in
 // registers across them) ------------------------------------------------------------------------------
+#ifdef RM_TIMING
+// phase timing of CTA 0 (debug builds only): cycles per phase slot, tools/fft_phase_timing.py
+#define FT_MARK(c) (c).t_mark = clock64()
+#define FT(c, slot)                                                            \
+  do {                                                                         \
+    const long long t_now_ = clock64();                                        \
+    if (blockIdx.x == 0 && threadIdx.x == 0) (c).P->timing[slot] += t_now_ - (c).t_mark; \
+    (c).t_mark = t_now_;                                                       \
+  } while (0)
+#else
+#define FT_MARK(c)
+#define FT(c, slot)
+#endif
+
 struct Ctx {
+#ifdef RM_TIMING
+  long long t_mark;
+#endif
   double* base;        // this chain's vectors
   const ChainArgs* P;
   int rank;
@@ -338,8 +371,13 @@ __device__ __forceinline__ double2* smem2() {
 __device__ __forceinline__ double2* SLOTS() { return smem2(); }
 __device__ __forceinline__ const double2* TW2() { return smem2() + NSLOT * SLOT; }
 __device__ __forceinline__ const double2* TW32() { return smem2() + NSLOT * SLOT + L; }
-__device__ __forceinline__ const double2* SYM() { return smem2() + NSLOT * SLOT + L + 16; }
-__device__ __forceinline__ double* WRED() { return reinterpret_cast<double*>(smem2() + NSLOT * SLOT + L + 16 + 6 * L); }
+// stiffness spectra (k-layout): per direction d (0 = x, 1 = y) the diagonal block's (real: T1 is symmetric)
+// and the off-diagonal block's; the third (transposed block) is its conjugate (rm_fft_symbols checks both)
+__device__ __forceinline__ const double* SYMR(int d) {
+  return reinterpret_cast<const double*>(smem2() + NSLOT * SLOT + L + 16) + d * L;
+}
+__device__ __forceinline__ const double2* SYMC(int d) { return smem2() + NSLOT * SLOT + L + 16 + L + d * L; }
+__device__ __forceinline__ double* WRED() { return reinterpret_cast<double*>(smem2() + NSLOT * SLOT + L + 16 + 3 * L); }
 // FP32 twiddles (tw2f[q * 32 + t] = W512^{q t}, tw32f[r] = W32^r) and the FP32 view of the slots
 __device__ __forceinline__ const float2* TW2F() { return reinterpret_cast<const float2*>(WRED() + 4 * 32); }
 __device__ __forceinline__ const float2* TW32F() { return TW2F() + L; }
@@ -413,9 +451,11 @@ __device__ __forceinline__ void col_pass_apply(Ctx& c) {
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
       const int e = r * 32 + c.lane();
-      double2 y = cmul(SYM()[3 * L + e], s0[e]);
-      y = cadd(y, cmul(SYM()[4 * L + e], sp[e]));
-      a[h][r] = cadd(y, cmul(SYM()[5 * L + e], sm[e]));
+      const double s0v = SYMR(1)[e];
+      const double2 s1v = SYMC(1)[e];
+      double2 y = cscale(s0[e], s0v);
+      y = cadd(y, cmul(s1v, sp[e]));
+      a[h][r] = cadd(y, cmulc(sm[e], s1v));
     }
   }
   __syncthreads();
@@ -474,13 +514,14 @@ __device__ __forceinline__ void row_pass_apply(Ctx& c, double (&acc)[NOWN][8], d
       for (int r = 0; r < 16; ++r) {
         const int e = r * 32 + c.lane();
         const double2 w = cscale(cmul(w0, TW32()[r]), sgn);  // e^{-i theta_k}
-        const double2 s0v = SYM()[e], s1v = SYM()[L + e], s2v = SYM()[2 * L + e];
-        const double2 c0 = make_double2(fma(sg, s0v.x, cm * (6.0 + 2.0 * w.x)), sg * s0v.y);
+        // c0 real (symmetric T1, tridiag(1,6,1)), c2 = conj(c1) (transposed block)
+        const double s0v = SYMR(0)[e];
+        const double2 s1v = SYMC(0)[e];
+        const double c0 = fma(sg, s0v, cm * (6.0 + 2.0 * w.x));
         const double2 c1 = make_double2(fma(sg, s1v.x, cm * (1.0 + w.x)), fma(sg, s1v.y, -cm * w.y));
-        const double2 c2 = make_double2(fma(sg, s2v.x, cm * (1.0 + w.x)), fma(sg, s2v.y, cm * w.y));
-        double2 y = cmul(c0, s0[e]);
+        double2 y = cscale(s0[e], c0);
         y = cadd(y, cmul(c1, sp[e]));
-        a[h][r] = cadd(y, cmul(c2, sm[e]));
+        a[h][r] = cadd(y, cmulc(sm[e], c1));
       }
     }
   }
@@ -499,12 +540,16 @@ __device__ __forceinline__ void row_pass_apply(Ctx& c, double (&acc)[NOWN][8], d
 
 // acc = (M + sg K) PV for the owner rows (PV complete and visible; one group barrier inside)
 __device__ __forceinline__ void apply_pv(Ctx& c, double (&acc)[NOWN][8], double sg) {
+  FT_MARK(c);
   col_pass_apply(c);
+  FT(c, 0);
   gsync(c.sy);
+  FT(c, 1);
   row_pass_apply(c, acc, sg);
   double wv[NOWN][8];
   RM_OWN_FOR { wv[p][m] = __ldcg(c.WV() + own_e(c, p, m)); }
   RM_OWN_FOR { acc[p][m] = own_valid(c, p, m) ? fma(sg, wv[p][m], acc[p][m]) : 0.0; }
+  FT(c, 2);
 }
 
 // refresh this CTA's 1/d(s) cache when s changed (once per sweep on uniform levels)
@@ -535,6 +580,7 @@ __device__ __forceinline__ void dinv_refresh(Ctx& c, double s) {
 // every stop is decided on the FP64 true residual -- and FP32 keeps it within ~1e-7 of the FP64 operator.
 __device__ __forceinline__ void precond(Ctx& c, const double (&r)[NOWN][8], double (&z)[NOWN][8], double s) {
   float2* slots = SLOTSF();
+  FT_MARK(c);
   dinv_refresh(c, s);
 #pragma unroll 1
   for (int h = 0; h < PPW; ++h) {  // SR[own rows] = Sx r (x-frequency along the row), pairs q = warp + WARPS h
@@ -555,7 +601,9 @@ __device__ __forceinline__ void precond(Ctx& c, const double (&r)[NOWN][8], doub
       }
     }
   }
+  FT(c, 5);
   gsync(c.sy);
+  FT(c, 6);
   {  // column pass: WV[:, own columns] = Sy diag(1/d) Sy SR
     for (int idx = c.tid(); idx < NP * H; idx += THREADS) {
       const int j = idx / H, q = idx % H;
@@ -590,7 +638,9 @@ __device__ __forceinline__ void precond(Ctx& c, const double (&r)[NOWN][8], doub
       c.WVf()[j * NP + c.C0() + q + H] = t.y;
     }
   }
+  FT(c, 7);
   gsync(c.sy);
+  FT(c, 8);
 #pragma unroll 1
   for (int h = 0; h < PPW; ++h) {  // z[own rows] = Sx WV[own rows]
     float2 a[16];
@@ -613,6 +663,7 @@ __device__ __forceinline__ void precond(Ctx& c, const double (&r)[NOWN][8], doub
       z[2 * h + 1][m] = own_valid(c, 2 * h + 1, m) ? (double)a[m].y : 0.0;
     }
   }
+  FT(c, 9);
 }
 
 __device__ __forceinline__ void put_pv(Ctx& c, const double (&v)[NOWN][8]) {
@@ -661,7 +712,7 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
   {
     double2* tw2 = const_cast<double2*>(TW2());    // tw2[q * 32 + t] = W512^{q t}
     double2* tw32 = const_cast<double2*>(TW32());  // W32^r = W512^{16 r}
-    double2* sym = const_cast<double2*>(SYM());    // 6 stiffness spectra in k-layout
+    double* sym = const_cast<double*>(SYMR(0));    // stiffness spectra (2 x 512 real, 2 x 512 complex)
     for (int i = tid; i < L; i += THREADS) {
       const int q = i >> 5, t = i & 31;
       double sn, cs;
@@ -675,7 +726,7 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
       tw32[tid] = make_double2(cs, sn);
       const_cast<float2*>(TW32F())[tid] = make_float2((float)cs, (float)sn);
     }
-    for (int i = tid; i < 6 * L; i += THREADS) sym[i] = P.fsym[i];
+    for (int i = tid; i < 6 * L; i += THREADS) sym[i] = P.fsym[i];  // 6 L doubles
   }
   const rm_sweep& W_ = P.sw;
   constexpr int nx = NX;
@@ -893,7 +944,9 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
           RM_OWN_FOR { p1[0] += pv[p][m] * ap[p][m]; }
         }
         double pap[1];
+        FT_MARK(c);
         creduce<1>(c, p1, pap);
+        FT(c, 3);
         if (!isfinite(pap[0]) || pap[0] <= 0.0) {
           fail = RM_CG_BREAKDOWN;
           its = k;
@@ -926,7 +979,9 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
             }
             part2[1] = part2[0];
           }
+          FT_MARK(c);
           creduce<2>(c, part2, red2);
+          FT(c, 10);
         }
         res = sqrt(red2[0]);
         if (!isfinite(res)) {
@@ -998,6 +1053,7 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
           }
         }
         gsync(c.sy);
+        FT(c, 11);
       }
 
       chain_ok = done && !fail && W_.x0_mode < 3;
@@ -1064,31 +1120,49 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
 
 #undef RM_OWN_FOR
 
-// Host: spectra of the six stiffness tables (entry d + np of table t, |d| < n used) in k-layout order:
-// out[2 (t L + r 32 + lane) + {0, 1}] = S_t[k], k = (lane >> 1) + 16 (r + 16 (lane & 1)).
-void fft_symbols(const double* tab, int np, int gl, double* out) {
+// Host: spectra of the stiffness tables (entry d + np of table t, |d| < n used) in k-layout order
+// (k = (lane >> 1) + 16 (r + 16 (lane & 1)), element e = r 32 + lane): out[0 .. 2L) = the real spectra of tables 0
+// (x) and 3 (y), out[2L .. 6L) = the complex spectra of tables 1 and 4.  Returns false unless tables 0 / 3 are
+// symmetric (real spectra) and tables 2 / 5 are the reversals of 1 / 4 (conjugate spectra), which the kernel
+// relies on (the Riesz generators, reference assembly.py:190-251, have both properties).
+bool fft_symbols(const double* tab, int np, int gl, double* out) {
   const int L = fft::L, n = np - 1;
   std::vector<double> cs(L), sn(L);
   for (int i = 0; i < L; ++i) {
     cs[i] = cos(2.0 * M_PI * i / L);
     sn[i] = sin(2.0 * M_PI * i / L);
   }
-  for (int t = 0; t < 6; ++t)
-    for (int r = 0; r < 16; ++r)
-      for (int lane = 0; lane < 32; ++lane) {
-        const int k = (lane >> 1) + 16 * (r + 16 * (lane & 1));
-        double re = 0.0, im = 0.0;
-        for (int d = -(n - 1); d <= n - 1; ++d) {
-          const double v = tab[t * gl + d + np];
-          if (v == 0.0) continue;
-          const int idx = (((d * k) % L) + L) % L;
-          re += v * cs[idx];
-          im -= v * sn[idx];
+  for (int d = 1; d < n; ++d)
+    for (int t = 0; t < 6; t += 3) {
+      if (tab[t * gl + np + d] != tab[t * gl + np - d]) return false;
+      if (tab[(t + 2) * gl + np + d] != tab[(t + 1) * gl + np - d] ||
+          tab[(t + 2) * gl + np - d] != tab[(t + 1) * gl + np + d])
+        return false;
+    }
+  for (int dir = 0; dir < 2; ++dir)
+    for (int which = 0; which < 2; ++which) {
+      const int t = 3 * dir + which;
+      for (int r = 0; r < 16; ++r)
+        for (int lane = 0; lane < 32; ++lane) {
+          const int k = (lane >> 1) + 16 * (r + 16 * (lane & 1));
+          double re = 0.0, im = 0.0;
+          for (int d = -(n - 1); d <= n - 1; ++d) {
+            const double v = tab[t * gl + d + np];
+            if (v == 0.0) continue;
+            const int idx = (((d * k) % L) + L) % L;
+            re += v * cs[idx];
+            im -= v * sn[idx];
+          }
+          const int e = r * 32 + lane;
+          if (which == 0) {
+            out[dir * L + e] = re;
+          } else {
+            out[2 * L + 2 * (dir * L + e)] = re;
+            out[2 * L + 2 * (dir * L + e) + 1] = im;
+          }
         }
-        const size_t e = (size_t)t * L + r * 32 + lane;
-        out[2 * e] = re;
-        out[2 * e + 1] = im;
-      }
+    }
+  return true;
 }
 
 bool fft_supported(int np, int nx, int ny) { return np == fft::NP && nx == fft::NP - 1 && ny == fft::NP - 1; }

@@ -30,7 +30,7 @@ struct ChainArgs {
   double lp_dmin, lp_kmin; // min over the grid of dm, dk: 1/(lp_dmin + s lp_kmin) bounds max 1/d(s)
   double gen_absmax;       // max |entry| of the six generator tables (split-FP16 table scaling)
   // FFT kernel (rm_fft.cu, 255^2 grids)
-  const double2* fsym;     // 6 stiffness spectra (512 points each), k-layout order
+  const double* fsym;      // stiffness spectra (rm_fft.cu fft_symbols): 2 x 512 real, 2 x 512 complex, k-layout
   double* fscratch;        // per-chain vectors (fft_scratch_doubles_per_chain each)
   const double* dmT;       // tau diagonals transposed, [nx][ny]
   const double* dkT;
@@ -74,7 +74,7 @@ int fft_group();
 size_t fft_scratch_doubles_per_chain();
 cudaError_t fft_max_chains(int* out);
 cudaError_t launch_fft(const ChainArgs& a, int max_chains, cudaStream_t st);
-void fft_symbols(const double* tab, int np, int gl, double* out_klayout);
+bool fft_symbols(const double* tab, int np, int gl, double* out_klayout);
 cudaError_t launch_diff_sqnorm(int64_t n, const double* a, const double* b, double* out, cudaStream_t st);
 
 }  // namespace rm

@@ -307,6 +307,13 @@ def cfg4_fullnt():
     _run_and_store("cfg4_fullnt.npz", "c4n", case, [0, 1, 7, 8, 1024, 4095, 4096, 8184, 8191, 8192])
 
 
+def cfg5_split():
+    """cfg5 grid and physics (1023^2, m=16) at the full run's step sizes: T = 32/65536, Nt = 32, i.e. fine
+    dt = 1/65536 and level-1 dt = 1/4096 (levels 32/2)."""
+    case = make_case("cfg5", Nt=32, T=32.0 / 65536)
+    _run_and_store("cfg5_split.npz", "c5p", case, [0, 1, 15, 16, 17, 31, 32])
+
+
 def pcg64():
     rng = np.random.default_rng(0)
     st = rng.bit_generator.state["state"]
@@ -324,7 +331,7 @@ if __name__ == "__main__":
            "pcg64": pcg64, "cfg1": cfg1, "reduced": reduced, "big": big,
            "big_tight": big_tight, "cfg2_full": cfg2_full, "cfg2_split": cfg2_split,
            "cfg3_split": cfg3_split, "cfg4_diverge": cfg4_diverge,
-           "cfg4_fullnt": cfg4_fullnt}
+           "cfg4_fullnt": cfg4_fullnt, "cfg5_split": cfg5_split}
     for w in which:
         t = time.perf_counter()
         fns[w]()
