@@ -280,16 +280,14 @@ __device__ __forceinline__ void gsync(Sync& sy) {
   __syncthreads();
   if (threadIdx.x == 0) {
     sy.epoch += 1;
-    __threadfence();
-    atomicAdd(sy.gbar, 1u);
+    // release-add: the CTA's writes (ordered before by the CTA barrier) become visible with the arrival
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(sy.gbar) : "memory");
     const unsigned target = sy.epoch * (unsigned)G;
     for (;;) {
       unsigned v;
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(sy.gbar) : "memory");
       if (v >= target) break;
-      __nanosleep(20);
     }
-    __threadfence();
   }
   __syncthreads();
 }
