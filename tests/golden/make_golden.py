@@ -314,6 +314,26 @@ def cfg5_split():
     _run_and_store("cfg5_split.npz", "c5p", case, [0, 1, 15, 16, 17, 31, 32])
 
 
+def theory_cases():
+    """Two-level bounds (reference theory.py:88-134) for cfg1, the cfg2 physics on 31^2 x 512 and the cfg4
+    physics on 63^2 graded x 512 (where the reference's MGRIT diverges)."""
+    from riesz_mgrit.theory import mode_spectrum, two_level_bound
+
+    out = {}
+    for tag, name, kw, m in (("t1", "cfg1", {}, 4), ("t2", "cfg2", dict(M=32, Nt=512), 8),
+                             ("t4", "cfg4", dict(M=64, Nt=512), 8)):
+        case = make_case(name, **kw)
+        spec = ref_spec(case)
+        sp = mode_spectrum(spec)
+        rep = two_level_bound(sp, spec.tmesh, m)
+        out[f"{tag}_sigmas"] = sp.sigmas
+        out[f"{tag}_bound"] = np.array(rep.bound)
+        out[f"{tag}_argmax"] = np.array(rep.argmax_mode)
+        out[f"{tag}_per_mode"] = rep.per_mode
+        print(tag, rep.bound, rep.argmax_mode, flush=True)
+    save("theory.npz", **out)
+
+
 def pcg64():
     rng = np.random.default_rng(0)
     st = rng.bit_generator.state["state"]
@@ -331,7 +351,8 @@ if __name__ == "__main__":
            "pcg64": pcg64, "cfg1": cfg1, "reduced": reduced, "big": big,
            "big_tight": big_tight, "cfg2_full": cfg2_full, "cfg2_split": cfg2_split,
            "cfg3_split": cfg3_split, "cfg4_diverge": cfg4_diverge,
-           "cfg4_fullnt": cfg4_fullnt, "cfg5_split": cfg5_split}
+           "cfg4_fullnt": cfg4_fullnt, "cfg5_split": cfg5_split,
+           "theory": theory_cases}
     for w in which:
         t = time.perf_counter()
         fns[w]()

@@ -140,3 +140,16 @@ def test_cfg2_full_matches_reference(golden, pre):
         assert abs(trace.cg_iterations[-1] - cg_ref[-1]) <= 0.01 * cg_ref[-1], (trace.cg_iterations[-1], cg_ref[-1])
     check_points(U, g, "c2f")
     np.testing.assert_allclose(trace.residual_norms, g["c2f_res"], rtol=1e-6, atol=0.2 * case.halt_tol)
+
+
+def test_cfg5_grid_in_the_full_run_regime_matches_reference(golden):
+    """cfg5 grid and physics (1023^2, m = 16) at the full run's step sizes (fine dt = 1/65536, coarse 1/4096;
+    two levels at Nt = 32) against the reference's own run: the NP = 1024 large-grid kernel."""
+    g = golden("cfg5_split.npz")
+    case = make_case("cfg5", Nt=32, T=32.0 / 65536)
+    opts = MgritOptions(m=case.m, max_levels=case.max_levels, halt_tol=case.halt_tol, cg_rel_tol=case.cg_rel_tol)
+    U, trace = solve(ProblemSpec(**case.problem_kwargs()), opts)
+    assert trace.converged
+    assert trace.iterations == int(g["c5p_its"])
+    assert np.array_equal(np.array(trace.spatial_solves), g["c5p_solves"])
+    check_points(U, g, "c5p")
