@@ -174,6 +174,10 @@ typedef struct rm_sweep {
      NULL: applied. */
   const double* d_ain;
   int64_t ain_stride;
+  /* optional: compressed G (uniform steps, time-separable source: G_n = tau_n A^-1 M g): every row n of
+     d_gadd and of d_hg is scaled by d_gscale[n] (pass them with stride 0 to store one vector each; the
+     reference computes G_n = rhs_vector(n) one solve at a time, mgrit.py:131-134).  NULL: rows as stored. */
+  const double* d_gscale;
 } rm_sweep;
 
 RM_API int rm_sweep_run(rm_grid* grid, const rm_sweep* sweep, void* stream);

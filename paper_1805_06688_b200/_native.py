@@ -49,6 +49,7 @@ class Sweep(C.Structure):
         ("d_ax", C.c_void_p), ("ax_stride", C.c_int64),
         ("d_gax", C.c_void_p), ("gax_stride", C.c_int64),
         ("d_ain", C.c_void_p), ("ain_stride", C.c_int64),
+        ("d_gscale", C.c_void_p),
     ]
 
 

@@ -631,6 +631,8 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
   const double cm = P.cm;
   const int64_t max_iter = W.max_iter > 0 ? W.max_iter : 10 * (int64_t)ndof;
   const bool need_in = W.explicit_rhs || W.x0_mode == 1;
+  // G row scale (compressed G, rm_sweep.d_gscale): rows of d_gadd / d_hg are d_gscale[n] times the stored row
+  auto gsc = [&](int k) -> double { return W.d_gscale ? W.d_gscale[k] : 1.0; };
   const bool fold_x = nx == C::NP - 1, fold_y = ny == C::NP - 1;  // even/odd folded DST stages
 
   if constexpr (PRE) {
@@ -701,7 +703,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
           const int fi = big_fidx(c, nf, e);
           double am = 0.0;
           if (j < ny && i < nx)
-            am = (1.0 + q) * big_mass<C>(pv0, j, i, cm) - q * (bs[fi] - rs[fi] + __ldcg(Hn + j * nx + i));
+            am = (1.0 + q) * big_mass<C>(pv0, j, i, cm) - q * (bs[fi] - rs[fi] + gsc(n - 1) * __ldcg(Hn + j * nx + i));
           acc[nf][e] = am;
         }
       }
@@ -737,7 +739,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
           double am = 0.0;
           if (j < ny && i < nx) {
             const int gi = j * nx + i;
-            am = (1.0 + q) * big_mass<C>(pv0, j, i, cm) - q * (__ldcg(An + gi) + __ldcg(Hn + gi));
+            am = (1.0 + q) * big_mass<C>(pv0, j, i, cm) - q * (__ldcg(An + gi) + gsc(n - 1) * __ldcg(Hn + gi));
           }
           acc[nf][e] = am;
         }
@@ -810,7 +812,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
             const int j = big_row(c, e), i = big_col(c, nf, e);
             if (j < ny && i < nx) {
               const int gi = j * nx + i;
-              put_tile(pv0, j, i, Gr ? __ldcg(gu + gi) - __ldcg(Gr + gi) : __ldcg(gu + gi));
+              put_tile(pv0, j, i, Gr ? __ldcg(gu + gi) - gsc(n) * __ldcg(Gr + gi) : __ldcg(gu + gi));
             }
           }
           big_sync<C>(sy);
@@ -837,7 +839,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
             double x0 = 0.0;
             if (j < ny && i < nx) {
               const int gi = j * nx + i;
-              x0 = Ax0 ? (Gr ? __ldcg(gu + gi) - __ldcg(Gr + gi) : __ldcg(gu + gi)) : __ldcg(pv0 + pv_idx<C>(j, i));
+              x0 = Ax0 ? (Gr ? __ldcg(gu + gi) - gsc(n) * __ldcg(Gr + gi) : __ldcg(gu + gi)) : __ldcg(pv0 + pv_idx<C>(j, i));
             }
             xs[fi] = x0;
             rs[fi] = acc[nf][e];
@@ -1128,7 +1130,7 @@ __global__ void __launch_bounds__(512, 1) chain_big_kernel(const ChainArgs P) {
           const int gi = j * nx + i;
           double y = xs[big_fidx(c, nf, e)];
           if (An) An[gi] = bs[big_fidx(c, nf, e)] - rs[big_fidx(c, nf, e)];  // A x = b - r (true residual)
-          if (Gn) y = __ldcg(Gn + gi) + y;
+          if (Gn) y = gsc(n) * __ldcg(Gn + gi) + y;
           if (Kn) Kn[gi] = y;
           if (Sn) y = y - __ldcg(Sn + gi);
           if (On) On[gi] = y;

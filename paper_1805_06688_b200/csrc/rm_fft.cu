@@ -731,6 +731,8 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
   c.di_s = __longlong_as_double(0x7ff8000000000000ll);  // NaN: nothing cached
   const int64_t max_iter = W_.max_iter > 0 ? W_.max_iter : 10 * (int64_t)NX * NX;
   const bool need_in = W_.explicit_rhs || W_.x0_mode == 1;
+  // G row scale (compressed G, rm_sweep.d_gscale): rows of d_gadd / d_hg are d_gscale[n] times the stored row
+  auto gsc = [&](int k) -> double { return W_.d_gscale ? W_.d_gscale[k] : 1.0; };
   c.base = P.fscratch + (size_t)cid * (NVEC * VEC + G * DIV);
   // zero this chain slot's vectors once (padding row / column 255 is never written afterwards)
   for (size_t i = (size_t)c.rank * THREADS + tid; i < NVEC * VEC; i += (size_t)G * THREADS) c.base[i] = 0.0;
@@ -776,7 +778,7 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
           const bool ok = own_valid(c, p, m);
           bv[p][m] = __ldcg(c.BV() + e);
           rv[p][m] = __ldcg(c.RV() + e);
-          hv[p][m] = ok ? __ldcg(Hn + own_j(c, p) * nx + own_i(c, m)) : 0.0;
+          hv[p][m] = ok ? gsc(n - 1) * __ldcg(Hn + own_j(c, p) * nx + own_i(c, m)) : 0.0;
         }
         RM_OWN_FOR {
           acc[p][m] = own_valid(c, p, m) ? (1.0 + q) * mv[p][m] - q * (bv[p][m] - rv[p][m] + hv[p][m]) : 0.0;
@@ -790,7 +792,7 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
           const int gi = own_j(c, p) * nx + own_i(c, m);
           const bool ok = own_valid(c, p, m);
           av[p][m] = ok ? __ldcg(An + gi) : 0.0;
-          hv[p][m] = ok ? __ldcg(Hn + gi) : 0.0;
+          hv[p][m] = ok ? gsc(n - 1) * __ldcg(Hn + gi) : 0.0;
         }
         RM_OWN_FOR { acc[p][m] = own_valid(c, p, m) ? (1.0 + q) * mv[p][m] - q * (av[p][m] + hv[p][m]) : 0.0; }
       } else if (need_in) {
@@ -866,7 +868,7 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
             double v = 0.0;
             if (own_valid(c, p, m)) {
               const int gi = own_j(c, p) * nx + own_i(c, m);
-              v = Gr ? __ldcg(gu + gi) - __ldcg(Gr + gi) : __ldcg(gu + gi);
+              v = Gr ? __ldcg(gu + gi) - gsc(n) * __ldcg(Gr + gi) : __ldcg(gu + gi);
             }
             g0[p][m] = v;
           }
@@ -1086,7 +1088,7 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
           const bool ok = own_valid(c, p, m);
           const int e = own_e(c, p, m), gi = own_j(c, p) * nx + own_i(c, m);
           xv[p][m] = __ldcg(c.XV() + e);
-          gv[p][m] = (Gn && ok) ? __ldcg(Gn + gi) : 0.0;
+          gv[p][m] = (Gn && ok) ? gsc(n) * __ldcg(Gn + gi) : 0.0;
           sv[p][m] = (Sn && ok) ? __ldcg(Sn + gi) : 0.0;
           bv[p][m] = An ? __ldcg(c.BV() + e) : 0.0;
           rv[p][m] = An ? __ldcg(c.RV() + e) : 0.0;

@@ -70,7 +70,7 @@ __device__ __forceinline__ int elem_sidx(const Ctx<C>& c, int mr, int nf, int e)
 // (the rows come from HBM or L2; a per-row loop would expose one latency per row)
 template <class C, bool SUB>
 __device__ __forceinline__ void load_rows(double* Vt, const double* __restrict__ a, const double* __restrict__ b,
-                                          int nx, int ny, const Ctx<C>& c) {
+                                          int nx, int ny, const Ctx<C>& c, double bs = 1.0) {
   constexpr int UN = SUB ? 4 : 8;
   const int ndof = nx * ny;
   for (int base = c.tid; base < ndof; base += C::THREADS * UN) {
@@ -86,7 +86,7 @@ __device__ __forceinline__ void load_rows(double* Vt, const double* __restrict__
       const int e = base + u * C::THREADS;
       if (e < ndof) {
         const int j = e / nx, i = e - j * nx;
-        Vt[vt_idx<C>(j, i)] = SUB ? va[u] - vb[u] : va[u];
+        Vt[vt_idx<C>(j, i)] = SUB ? va[u] - bs * vb[u] : va[u];
       }
     }
   }
@@ -101,9 +101,9 @@ __device__ __forceinline__ void load_vec(double* Vt, const double* __restrict__ 
 // Vt <- guess - G (G may be null)
 template <class C>
 __device__ __forceinline__ void load_guess(double* Vt, const double* __restrict__ guess, const double* __restrict__ G,
-                                           int nx, int ny, const Ctx<C>& c) {
+                                           int nx, int ny, const Ctx<C>& c, double gs) {
   if (G)
-    load_rows<C, true>(Vt, guess, G, nx, ny, c);
+    load_rows<C, true>(Vt, guess, G, nx, ny, c, gs);
   else
     load_rows<C, false>(Vt, guess, nullptr, nx, ny, c);
 }
@@ -489,6 +489,8 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
   const double cm = P.cm;
   const int64_t max_iter = W.max_iter > 0 ? W.max_iter : 10 * (int64_t)ndof;
   const bool need_in = W.explicit_rhs || W.x0_mode == 1;
+  // G row scale (compressed G, rm_sweep.d_gscale): rows of d_gadd / d_hg are d_gscale[n] times the stored row
+  auto gsc = [&](int k) -> double { return W.d_gscale ? W.d_gscale[k] : 1.0; };
 
   for (int i = c.tid; i < C::VT; i += C::THREADS) Vt[i] = 0.0;
   if constexpr (PRE) {
@@ -627,7 +629,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           double am = 0.0;
           if (j < ny && i < nx) {
             const int gi = j * nx + i;
-            am = (1.0 + q) * mass_stencil<C>(Vt, j, i, cm) - q * (__ldcg(An + gi) + __ldcg(Hn + gi));
+            am = (1.0 + q) * mass_stencil<C>(Vt, j, i, cm) - q * (__ldcg(An + gi) + gsc(n - 1) * __ldcg(Hn + gi));
           }
           acc[mr][nf][e] = am;
         }
@@ -640,7 +642,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           const int j = elem_row<C>(c, mr, e), i = elem_col<C>(c, nf, e);
           double am = 0.0;
           if (j < ny && i < nx) {
-            const double ax = sb_[elem_sidx<C>(c, mr, nf, e)] - rr_[mr][nf][e] + __ldcg(Hn + j * nx + i);
+            const double ax = sb_[elem_sidx<C>(c, mr, nf, e)] - rr_[mr][nf][e] + gsc(n - 1) * __ldcg(Hn + j * nx + i);
             am = (1.0 + q) * mass_stencil<C>(Vt, j, i, cm) - q * ax;
           }
           acc[mr][nf][e] = am;
@@ -716,7 +718,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
         // operator whose A x was stored (d_gax) -- read back: no apply
         const double* Ax0 = W.d_gax ? W.d_gax + (int64_t)n * W.gax_stride : nullptr;
         if (!Ax0) {
-          load_guess<C>(Vt, Gu, Gr, nx, ny, c);
+          load_guess<C>(Vt, Gu, Gr, nx, ny, c, gsc(n));
           __syncthreads();
           matvec<C>(Vt, gens, acc, c.urow, c.ucol, c.gq, c.tig, kx_end, ky_end, true, true, P.merge);
           ++nmv;
@@ -741,7 +743,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
             double x0 = 0.0;
             if (j < ny && i < nx) {
               if (Ax0)
-                x0 = Gr ? __ldcg(Gu + j * nx + i) - __ldcg(Gr + j * nx + i) : __ldcg(Gu + j * nx + i);
+                x0 = Gr ? __ldcg(Gu + j * nx + i) - gsc(n) * __ldcg(Gr + j * nx + i) : __ldcg(Gu + j * nx + i);
               else
                 x0 = Vt[vt_idx<C>(j, i)];
             }
@@ -1120,7 +1122,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) chain_kernel(const ChainArgs P)
           const int gi = j * nx + i;
           double y = xs[elem_xidx<C>(c, mr, nf, e)];
           if (An) An[gi] = sb_[elem_sidx<C>(c, mr, nf, e)] - rr_[mr][nf][e];  // A x = b - r (true residual)
-          if (Gn) y = __ldcg(Gn + gi) + y;
+          if (Gn) y = gsc(n) * __ldcg(Gn + gi) + y;
           if (Kn) Kn[gi] = y;
           if (Sn) y = y - __ldcg(Sn + gi);
           if (On) On[gi] = y;

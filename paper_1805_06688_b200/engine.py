@@ -191,8 +191,12 @@ class Engine:
               max_iter: int | None = None, group: int = 0, row: int | None = None, tag: str = "",
               precond: str = "none", guess=None, keep: torch.Tensor | None = None,
               hg: torch.Tensor | None = None, ax: torch.Tensor | None = None,
-              gax: torch.Tensor | None = None, ain: torch.Tensor | None = None) -> None:
-        """One rm_sweep_run launch; 2-D arrays are indexed by time point with row stride ``row``."""
+              gax: torch.Tensor | None = None, ain: torch.Tensor | None = None,
+              gscale: torch.Tensor | None = None) -> None:
+        """One rm_sweep_run launch; 2-D arrays are indexed by time point with row stride ``row``.
+
+        ``gscale`` (compressed G): ``gadd`` and ``hg`` are single vectors, row n of each is gscale[n] times it.
+        """
         if nchains <= 0:
             return
         row = self.ndof if row is None else row
@@ -213,6 +217,10 @@ class Engine:
         sw.d_guess, sw.guess_stride = _ptr(guess, row), row
         sw.d_keep, sw.keep_stride = _ptr(keep, row), row
         sw.d_hg, sw.hg_stride = _ptr(hg, row), row
+        if gscale is not None:  # one stored vector each, scaled per row by gscale[n]
+            sw.d_gadd, sw.gadd_stride = _ptr(gadd), 0
+            sw.d_hg, sw.hg_stride = _ptr(hg), 0
+            sw.d_gscale = _ptr(gscale, 1)
         sw.d_ax, sw.ax_stride = _ptr(ax, row), row
         sw.d_gax, sw.gax_stride = _ptr(gax, row), row
         sw.d_ain, sw.ain_stride = _ptr(ain, row), row

@@ -23,31 +23,57 @@ from paper_1805_06688_b200.stepper import ProblemSpec
 from paper_1805_06688_b200.timeslab import make_plan
 
 
-def test_plan_aligned_partition():
-    # cfg2 structure: 4096 / 512 / 64 / 8 points, m = 8 -> blocks of 512 fine steps
-    plan = make_plan([4096, 512, 64, 8], 8, 8, 3)
-    assert plan.own(0) == (1536, 2048)
-    assert plan.own(1) == (192, 256)
-    assert plan.own(2) == (24, 32)
-    assert plan.own(3) == (3, 4)
-    assert plan.left_source(0) == 2 and plan.right_targets(0) == [4]
-    assert plan.owner(3, 0) == 0 and plan.owner(3, 8) == 7
-    with pytest.raises(ValueError, match="aligned"):
-        make_plan([4096, 512, 64, 8], 8, 16, 0)
-    # uneven split: 3 ranks over 8 blocks
+def test_plan_distributes_the_deepest_feasible_prefix():
+    # cfg3 structure: 16384 / 1024 / 64 / 4 points, m = 16
+    pts3 = [16384, 1024, 64, 4]
+    p8 = make_plan(pts3, 16, 8, 3)
+    assert p8.n_dist == 2  # 64 intervals of level 1 >= 8 ranks; level 2 has only 4
+    assert p8.own(0) == (6144, 8192) and p8.own(1) == (384, 512)
+    assert p8.own(2) == (0, 0) and make_plan(pts3, 16, 8, 0).own(2) == (0, 64)  # gathered on rank 0
+    assert p8.left_source(0) == 2 and p8.right_targets(0) == [4] and p8.left_source(2) is None
+    assert make_plan(pts3, 16, 4, 0).n_dist == 3 and make_plan(pts3, 16, 2, 1).n_dist == 3
+    # cfg4 structure: 8192 / 1024 / 128 / 16 / 2, m = 8: 8 ranks keep three distributed levels
+    assert make_plan([8192, 1024, 128, 16, 2], 8, 8, 0).n_dist == 3
+    # cfg2 at 8 ranks
+    p = make_plan([4096, 512, 64, 8], 8, 8, 3)
+    assert p.n_dist == 3 and p.own(0) == (1536, 2048) and p.own(2) == (24, 32)
+    with pytest.raises(ValueError, match="intervals"):
+        make_plan([4096, 512, 64, 8], 8, 1024, 0)
+    # uneven split: 3 ranks
     p3 = [make_plan([4096, 512, 64, 8], 8, 3, r).own(0) for r in range(3)]
     assert p3[0][0] == 0 and p3[-1][1] == 4096
     assert all(a[1] == b[0] for a, b in zip(p3, p3[1:]))
     assert all((hi - lo) % 512 == 0 for lo, hi in p3)
 
 
-def _spec():
+def test_cfg5_slab_memory_fits_8_gpus():
+    """cfg5 (1023^2 DOF, 65536 steps, m = 16) at 8 ranks: with slab-local rows and the compressed G (one vector
+    plus N scalars) every rank's device arrays fit a 180 GB B200 -- U's slab alone is BASELINE's ~64 GB per GPU
+    (68.7 GB) -- where full-length arrays would take 1.1 TB per rank and an uncompressed G another 68.7 GB."""
+    from paper_1805_06688_b200.timeslab import slab_bytes
+
+    pts = [65536, 4096, 256, 16]
+    ndof = 1023 * 1023
+    per_rank = [slab_bytes(make_plan(pts, 16, 8, r), ndof) for r in range(8)]
+    u_slab = (65536 // 8 + 1) * ndof * 8
+    assert u_slab / 1e9 == pytest.approx(68.6, abs=0.2)
+    assert max(per_rank) <= 1.3 * u_slab < 100e9, [b / 1e9 for b in per_rank]
+    uncompressed = [slab_bytes(make_plan(pts, 16, 8, r), ndof, compressed_g=False) for r in range(8)]
+    assert min(uncompressed) - max(per_rank) > 0.9 * u_slab  # the compression saves one fine-level array
+    full_length = 65537 * ndof * 8 * 2
+    assert max(per_rank) < full_length / 10
+
+
+def _spec(M=6, N=64):
     c = manufactured()
-    return ProblemSpec(SpatialGrid(6, 6), uniform_temporal(1.0, 64), c["kx"], c["ky"], c["beta"], c["gamma"],
+    return ProblemSpec(SpatialGrid(M, M), uniform_temporal(1.0, N), c["kx"], c["ky"], c["beta"], c["gamma"],
                        c["source"], c["initial"])
 
 
 OPTS = {
+    # four levels (256/64/16/4, m = 4) with the device's reuse inputs on (second guess, apply-free right-hand
+    # sides, stored A x, kept C-points): at 8 ranks levels 2 and 3 are gathered on rank 0
+    "deep": dict(m=4, halt_tol=1e-10, cg_rel_tol=1e-12, cg_preconditioner="tau"),
     "multi": dict(m=4, halt_tol=1e-10, cg_rel_tol=1e-12, cg_preconditioner="none"),
     "two": dict(m=4, max_levels=2, halt_tol=1e-10, cg_rel_tol=1e-12, cg_preconditioner="none"),
     "noskip_f": dict(m=2, halt_tol=1e-10, cg_rel_tol=1e-12, relaxation="f", skip_first_down=False,
@@ -59,7 +85,13 @@ def _run(tag, distributed):
     sys.path.insert(0, os.path.join(REPO, "tests"))
     from cpu_engine import cpu_disc_factory
 
-    U, tr = solve(_spec(), MgritOptions(**OPTS[tag]), disc_factory=cpu_disc_factory, distributed=distributed)
+    if tag == "deep":  # cfg2-type separable source on a uniform grid: the compressed G path
+        from paper_1805_06688_b200.configs import make_case
+
+        spec = ProblemSpec(**make_case("cfg2", M=4, Nt=256).problem_kwargs())
+    else:
+        spec = _spec()
+    U, tr = solve(spec, MgritOptions(**OPTS[tag]), _disc_factory=cpu_disc_factory, distributed=distributed)
     return U, tr
 
 
@@ -82,7 +114,8 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world,tags", [(2, ("multi", "two", "noskip_f")), (4, ("multi",))])
+@pytest.mark.parametrize("world,tags", [(2, ("multi", "two", "noskip_f", "deep")), (4, ("multi", "deep")),
+                                        (8, ("deep",))])
 def test_distributed_trace_bitwise_equal(world, tags):
     single = {tag: _run(tag, False) for tag in tags}
     ctx = mp.get_context("spawn")
@@ -100,7 +133,10 @@ def test_distributed_trace_bitwise_equal(world, tags):
         assert res == tr1.residual_norms, (tag, rank)
         assert solves == tr1.spatial_solves, (tag, rank)
         assert cgits == tr1.cg_iterations, (tag, rank)
-        assert np.array_equal(U, U1), (tag, rank)
+        if rank == 0:  # the assembled host result (other ranks return None)
+            assert np.array_equal(U, U1), (tag, rank)
+        else:
+            assert U is None
 
 
 OPTS["noskip_fcf"] = dict(m=4, halt_tol=1e-10, cg_rel_tol=1e-12, skip_first_down=False, cg_preconditioner="none")
@@ -121,6 +157,8 @@ def test_single_rank_driver_matches_oracle(tag):
     R, rtr = O.mgrit_solve(prob, O.Options(**o))
     assert tr.iterations == rtr.iterations
     assert tr.spatial_solves == rtr.spatial_solves
-    assert tr.cg_iterations == rtr.cg_iterations
-    np.testing.assert_allclose(tr.residual_norms, rtr.residual_norms, rtol=1e-9)
+    # the apply-free chain right-hand sides (rm_sweep d_hg / d_ain, mirrored by the CPU engine) are exact up to
+    # rounding, which can move a solve's last CG iteration across the tolerance: counts agree to 0.1 %
+    assert all(abs(a - b) <= 1e-3 * b + 2 for a, b in zip(tr.cg_iterations, rtr.cg_iterations))
+    np.testing.assert_allclose(tr.residual_norms, rtr.residual_norms, rtol=1e-9, atol=1e-3 * OPTS[tag]["halt_tol"])
     np.testing.assert_allclose(U, R, rtol=0, atol=1e-13 * np.abs(R).max())
