@@ -74,7 +74,13 @@ def build(force: bool = False, verbose: bool = False, timing: bool = False) -> s
     os.makedirs(LIBDIR, exist_ok=True)
     extra = ["-DRM_TIMING"] if timing else []
     extra += [f"-D{d}" for d in os.environ.get("RM_DEFINES", "").split(",") if d]
-    objdir = tempfile.mkdtemp(prefix="rm_build_", dir=LIBDIR)  # private: concurrent builds do not collide
+    cache = os.environ.get("RM_OBJ_CACHE")  # developer option: keep objects, recompile stale sources only
+    if cache:
+        objdir = os.path.join(cache, "timing" if timing else "plain")
+        os.makedirs(objdir, exist_ok=True)
+    else:
+        objdir = tempfile.mkdtemp(prefix="rm_build_", dir=LIBDIR)  # private: concurrent builds do not collide
+    deps = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(REPO, "include", "riesz_mgrit_b200.h")]
     jobs = []  # (label, source, defines, object)
     for src in SOURCES:
         jobs.append((src, src, [], os.path.join(objdir, src.replace(".cu", ".o"))))
@@ -87,10 +93,16 @@ def build(force: bool = False, verbose: bool = False, timing: bool = False) -> s
     while pending or running:
         while pending and len(running) < nproc:
             label, src, defs, obj = pending.pop(0)
+            if cache and os.path.exists(obj) and all(
+                    os.path.getmtime(f) < os.path.getmtime(obj) for f in deps + [os.path.join(CSRC, src)]):
+                objs.append(obj)
+                continue
             cmd = [nvcc(), *NVCC_FLAGS, *extra, *defs, "-I", os.path.join(REPO, "include"), "-I", CSRC, "-c",
                    os.path.join(CSRC, src), "-o", obj]
             running.append((label, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
                                                          text=True)))
+        if not running:
+            continue
         label, obj, proc = running.pop(0)
         _, err = proc.communicate()
         if proc.returncode != 0:
@@ -106,9 +118,10 @@ def build(force: bool = False, verbose: bool = False, timing: bool = False) -> s
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stderr}")
     os.replace(tmp, out)
-    for o in objs:
-        os.remove(o)
-    os.rmdir(objdir)
+    if not cache:
+        for o in objs:
+            os.remove(o)
+        os.rmdir(objdir)
     return out
 
 

@@ -332,6 +332,19 @@ __device__ __forceinline__ void greduce(double (&part)[NV], double* wred, Sync& 
 #define FT_MARK(c)
 #define FT(c, slot)
 #endif
+#if defined(RM_TIMING) && defined(RM_TIMING_FINE)
+// sub-phase slots of the two apply passes (replace the coarse slots: -DRM_TIMING,RM_TIMING_FINE)
+#undef FT
+#define FT(c, slot)
+#define FTF(c, slot)                                                           \
+  do {                                                                         \
+    const long long t_now_ = clock64();                                        \
+    if (blockIdx.x == 0 && threadIdx.x == 0) (c).P->timing[slot] += t_now_ - (c).t_mark; \
+    (c).t_mark = t_now_;                                                       \
+  } while (0)
+#else
+#define FTF(c, slot)
+#endif
 
 struct Ctx {
 #ifdef RM_TIMING
@@ -414,81 +427,16 @@ __device__ __forceinline__ void mass_own(const Ctx& c, double (&out)[NOWN][8]) {
   }
 }
 
-// y-direction pass of the stiffness: WV[:, own columns] = (1/L) sum_t IFFT(S_t FFT(PV columns i + 0/+1/-1))
-__device__ __forceinline__ void col_pass_apply(Ctx& c) {
+// forward FFTs of a pass's packed pairs: the two halo slots first (warps 0 and WARPS-1, which are the warps
+// whose output pair couples to them), then every warp its own pair (slot warp + 1), whose spectrum stays in
+// registers for the combination; LOAD(s, a) fills a[0..8) with the pair of slot s (a[8..16) = 0: zero padding
+// known at compile time, so the first radix stage is pruned)
+template <class LOAD>
+__device__ __forceinline__ void forward_pairs(Ctx& c, double2 (&a)[16], LOAD load) {
   double2* slots = SLOTS();
-  // stage columns C0-1 .. C0+32 into slots s = 0..17 (pair (C0+s-1, C0+s+15)), natural row order; a warp
-  // covers 34 consecutive columns of one row per step (coalesced)
-  // stage columns C0-1 .. C0+32: slot s = (column C0+s-1, column C0+s+15), one 16-byte store per element pair
-  for (int idx = c.tid(); idx < NP * NSLOT; idx += THREADS) {
-    const int j = idx / NSLOT, s = idx - j * NSLOT;
-    const int ca = c.C0() + s - 1, cb = c.C0() + s + H - 1;
-    const double* row = c.PV() + j * NP;
-    slots[s * SLOT + j] = make_double2(ca >= 0 ? __ldcg(row + ca) : 0.0, cb < NP ? __ldcg(row + cb) : 0.0);
-  }
-  for (int idx = c.tid(); idx < NSLOT * (L - NP); idx += THREADS)
-    slots[(idx / (L - NP)) * SLOT + NP + idx % (L - NP)] = make_double2(0.0, 0.0);
-  __syncthreads();
-  for (int s = c.warp(); s < NSLOT; s += WARPS) {
-    double2 a[16];
-    double2* sl = slots + s * SLOT;
-#pragma unroll
-    for (int m = 0; m < 16; ++m) a[m] = sl[c.lane() + 32 * m];
-    fft512_fwd(a, sl, TW2(), TW32(), c.lane());
-    __syncwarp();
-#pragma unroll
-    for (int r = 0; r < 16; ++r) sl[r * 32 + c.lane()] = a[r];
-  }
-  __syncthreads();
-  double2 a[PPW][16];  // output pairs q = warp + WARPS h
-#pragma unroll
-  for (int h = 0; h < PPW; ++h) {
-    const double2* s0 = slots + (c.warp() + WARPS * h + 1) * SLOT;  // columns i
-    const double2* sp = s0 + SLOT;                              // columns i + 1
-    const double2* sm = s0 - SLOT;                              // columns i - 1
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      const int e = r * 32 + c.lane();
-      const double s0v = SYMR(1)[e];
-      const double2 s1v = SYMC(1)[e];
-      double2 y = cscale(s0[e], s0v);
-      y = cadd(y, cmul(s1v, sp[e]));
-      a[h][r] = cadd(y, cmulc(sm[e], s1v));
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int h = 0; h < PPW; ++h) {
-    double2* sl = slots + (c.warp() + WARPS * h + 1) * SLOT;
-    fft512_inv(a[h], sl, TW2(), TW32(), c.lane());
-    __syncwarp();
-    constexpr double inv_l = 1.0 / (double)L;
-#pragma unroll
-    for (int m = 0; m < 8; ++m) sl[c.lane() + 32 * m] = cscale(a[h][m], inv_l);
-  }
-  __syncthreads();
-  // store the 32 own columns, one row per warp step
-  for (int idx = c.tid(); idx < NP * H; idx += THREADS) {
-    const int j = idx / H, q = idx % H;
-    const double2 t = slots[(q + 1) * SLOT + j];
-    c.WV()[j * NP + c.C0() + q] = t.x;
-    c.WV()[j * NP + c.C0() + q + H] = t.y;
-  }
-}
-
-// x-direction pass for the owner rows with the P1 mass folded in: acc = (1/L) sum_t IFFT((sg S_t + cm M_t) FFT(PV
-// rows j + 0/+1/-1)); the mass blocks tridiag(1,6,1), (1 at d = 0,-1), (1 at d = 0,+1) have the spectra
-// 6 + 2 cos(theta), 1 + e^{i theta}, 1 + e^{-i theta}, theta = 2 pi k / L (rm_device.cuh build_step_tables)
-__device__ __forceinline__ void row_pass_apply(Ctx& c, double (&acc)[NOWN][8], double sg) {
-  double2* slots = SLOTS();
-  for (int s = c.warp(); s < NSLOT; s += WARPS) {
-    const int ja = c.R0() + s - 1, jb = c.R0() + s - 1 + H;
-    double2 a[16];
-    const double* ra = c.PV() + ja * NP + c.lane();
-    const double* rb = c.PV() + jb * NP + c.lane();
-    const bool va = ja >= 0, vb = jb < NP;
-#pragma unroll
-    for (int m = 0; m < 8; ++m) a[m] = make_double2(va ? __ldcg(ra + 32 * m) : 0.0, vb ? __ldcg(rb + 32 * m) : 0.0);
+  if (c.warp() == 0 || c.warp() == WARPS - 1) {
+    const int s = c.warp() == 0 ? 0 : NSLOT - 1;
+    load(s, a);
 #pragma unroll
     for (int m = 8; m < 16; ++m) a[m] = make_double2(0.0, 0.0);
     double2* sl = slots + s * SLOT;
@@ -497,57 +445,205 @@ __device__ __forceinline__ void row_pass_apply(Ctx& c, double (&acc)[NOWN][8], d
 #pragma unroll
     for (int r = 0; r < 16; ++r) sl[r * 32 + c.lane()] = a[r];
   }
-  __syncthreads();
-  double2 a[PPW][16];  // output pairs q = warp + WARPS h
-  {
-    const double2 w0 = TW2()[32 + (c.lane() >> 1)];  // W512^{q}
-    const double sgn = (c.lane() & 1) ? -1.0 : 1.0;   // W512^{256 v}
-    const double cm = c.P->cm;
+  const int s = c.warp() + 1;
+  load(s, a);
 #pragma unroll
-    for (int h = 0; h < PPW; ++h) {
-      const double2* s0 = slots + (c.warp() + WARPS * h + 1) * SLOT;
-      const double2* sp = s0 + SLOT;
-      const double2* sm = s0 - SLOT;
+  for (int m = 8; m < 16; ++m) a[m] = make_double2(0.0, 0.0);
+  double2* sl = slots + s * SLOT;
+  fft512_fwd(a, sl, TW2(), TW32(), c.lane());
+  __syncwarp();
 #pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        const int e = r * 32 + c.lane();
-        const double2 w = cscale(cmul(w0, TW32()[r]), sgn);  // e^{-i theta_k}
-        // c0 real (symmetric T1, tridiag(1,6,1)), c2 = conj(c1) (transposed block)
-        const double s0v = SYMR(0)[e];
-        const double2 s1v = SYMC(0)[e];
-        const double c0 = fma(sg, s0v, cm * (6.0 + 2.0 * w.x));
-        const double2 c1 = make_double2(fma(sg, s1v.x, cm * (1.0 + w.x)), fma(sg, s1v.y, -cm * w.y));
-        double2 y = cscale(s0[e], c0);
-        y = cadd(y, cmul(c1, sp[e]));
-        a[h][r] = cadd(y, cmulc(sm[e], c1));
+  for (int r = 0; r < 16; ++r) sl[r * 32 + c.lane()] = a[r];
+}
+
+// y-direction pass of the stiffness: WV[:, own columns] = (1/L) sum_t IFFT(S_t FFT(PV columns i + 0/+1/-1)).
+// DOT: also returns this thread's share of sum PV .* WV over the own columns (the y-part of p.Ap, summed by
+// the column owners so that the group reduction of p.Ap is the barrier that publishes WV)
+template <bool DOT>
+__device__ __forceinline__ double col_pass_apply(Ctx& c) {
+  static_assert(PPW == 1 && (NP * NSLOT) % THREADS == 0 && (NP * H) % THREADS == 0, "pass geometry");
+  double2* slots = SLOTS();
+  {  // stage columns C0-1 .. C0+32: slot s = (column C0+s-1, column C0+s+15), natural row order; the loads of a
+     // batch are issued before its first store
+    constexpr int NIT = NP * NSLOT / THREADS, NB = 3;
+    static_assert(NIT % NB == 0, "staging batches");
+#pragma unroll 1
+    for (int it0 = 0; it0 < NIT; it0 += NB) {
+      double2 v[NB];
+#pragma unroll
+      for (int it = 0; it < NB; ++it) {
+        const int idx = c.tid() + (it0 + it) * THREADS;
+        const int j = idx / NSLOT, s = idx - j * NSLOT;
+        const int ca = c.C0() + s - 1, cb = c.C0() + s + H - 1;
+        const double* row = c.PV() + j * NP;
+        v[it] = make_double2(ca >= 0 ? __ldcg(row + ca) : 0.0, cb < NP ? __ldcg(row + cb) : 0.0);
+      }
+#pragma unroll
+      for (int it = 0; it < NB; ++it) {
+        const int idx = c.tid() + (it0 + it) * THREADS;
+        const int j = idx / NSLOT, s = idx - j * NSLOT;
+        slots[s * SLOT + j] = v[it];
       }
     }
   }
   __syncthreads();
-  constexpr double inv_l = 1.0 / (double)L;
+  FTF(c, 0);
+  double2 a[16];  // own pair q = warp
+  forward_pairs(c, a, [&](int s, double2 (&x)[16]) {
+    const double2* sl = slots + s * SLOT;
 #pragma unroll
-  for (int h = 0; h < PPW; ++h) {
-    fft512_inv(a[h], slots + (c.warp() + WARPS * h + 1) * SLOT, TW2(), TW32(), c.lane());
+    for (int m = 0; m < 8; ++m) x[m] = sl[c.lane() + 32 * m];
+    __syncwarp();  // (the slot doubles as the transform's transpose scratch)
+  });
+  __syncthreads();
+  FTF(c, 1);
+  {
+    const double2* s0 = slots + (c.warp() + 1) * SLOT;  // columns i
+    const double2* sp = s0 + SLOT;                      // columns i + 1
+    const double2* sm = s0 - SLOT;                      // columns i - 1
 #pragma unroll
-    for (int m = 0; m < 8; ++m) {
-      acc[2 * h][m] = a[h][m].x * inv_l;
-      acc[2 * h + 1][m] = a[h][m].y * inv_l;
+    for (int r = 0; r < 16; ++r) {
+      const int e = r * 32 + c.lane();
+      const double s0v = SYMR(1)[e];
+      const double2 s1v = SYMC(1)[e];
+      double2 y = cscale(a[r], s0v);
+      y = cadd(y, cmul(s1v, sp[e]));
+      a[r] = cadd(y, cmulc(sm[e], s1v));
     }
   }
+  __syncthreads();
+  FTF(c, 2);
+  {
+    double2* sl = slots + (c.warp() + 1) * SLOT;
+    fft512_inv(a, sl, TW2(), TW32(), c.lane());
+    __syncwarp();
+    constexpr double inv_l = 1.0 / (double)L;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) sl[c.lane() + 32 * m] = cscale(a[m], inv_l);
+  }
+  __syncthreads();
+  FTF(c, 3);
+  // store the 32 own columns, one row per half-warp step
+  double dot = 0.0;
+  {
+    constexpr int NIT = NP * H / THREADS, NB = 4;
+    static_assert(NIT % NB == 0, "store batches");
+#pragma unroll 1
+    for (int it0 = 0; it0 < NIT; it0 += NB) {
+      double2 pv[NB];
+      if constexpr (DOT) {
+#pragma unroll
+        for (int it = 0; it < NB; ++it) {
+          const int idx = c.tid() + (it0 + it) * THREADS;
+          const int j = idx / H, q = idx % H;
+          const double* row = c.PV() + j * NP + c.C0() + q;
+          pv[it] = make_double2(__ldcg(row), __ldcg(row + H));
+        }
+      }
+#pragma unroll
+      for (int it = 0; it < NB; ++it) {
+        const int idx = c.tid() + (it0 + it) * THREADS;
+        const int j = idx / H, q = idx % H;
+        const double2 t = slots[(q + 1) * SLOT + j];
+        c.WV()[j * NP + c.C0() + q] = t.x;
+        c.WV()[j * NP + c.C0() + q + H] = t.y;
+        if constexpr (DOT) dot = fma(pv[it].x, t.x, fma(pv[it].y, t.y, dot));
+      }
+    }
+  }
+  FTF(c, 4);
+  return dot;
+}
+
+// x-direction pass for the owner rows with the P1 mass folded in: acc = (1/L) sum_t IFFT((sg S_t + cm M_t) FFT(PV
+// rows j + 0/+1/-1)); the mass blocks tridiag(1,6,1), (1 at d = 0,-1), (1 at d = 0,+1) have the spectra
+// 6 + 2 cos(theta), 1 + e^{i theta}, 1 + e^{-i theta}, theta = 2 pi k / L (rm_device.cuh build_step_tables)
+__device__ __forceinline__ void row_pass_apply(Ctx& c, double (&acc)[NOWN][8], double sg) {
+  double2* slots = SLOTS();
+  double2 a[16];  // own pair q = warp
+  forward_pairs(c, a, [&](int s, double2 (&x)[16]) {
+    const int ja = c.R0() + s - 1, jb = c.R0() + s - 1 + H;
+    const double* ra = c.PV() + ja * NP + c.lane();
+    const double* rb = c.PV() + jb * NP + c.lane();
+    const bool va = ja >= 0, vb = jb < NP;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) x[m] = make_double2(va ? __ldcg(ra + 32 * m) : 0.0, vb ? __ldcg(rb + 32 * m) : 0.0);
+  });
+  __syncthreads();
+  FTF(c, 6);
+  {
+    const double2 w0 = TW2()[32 + (c.lane() >> 1)];  // W512^{q}
+    const double sgn = (c.lane() & 1) ? -1.0 : 1.0;   // W512^{256 v}
+    const double cm = c.P->cm;
+    const double2* s0 = slots + (c.warp() + 1) * SLOT;
+    const double2* sp = s0 + SLOT;
+    const double2* sm = s0 - SLOT;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const int e = r * 32 + c.lane();
+      const double2 w = cscale(cmul(w0, TW32()[r]), sgn);  // e^{-i theta_k}
+      // c0 real (symmetric T1, tridiag(1,6,1)), c2 = conj(c1) (transposed block)
+      const double s0v = SYMR(0)[e];
+      const double2 s1v = SYMC(0)[e];
+      const double c0 = fma(sg, s0v, cm * (6.0 + 2.0 * w.x));
+      const double2 c1 = make_double2(fma(sg, s1v.x, cm * (1.0 + w.x)), fma(sg, s1v.y, -cm * w.y));
+      double2 y = cscale(a[r], c0);
+      y = cadd(y, cmul(c1, sp[e]));
+      a[r] = cadd(y, cmulc(sm[e], c1));
+    }
+  }
+  __syncthreads();
+  FTF(c, 7);
+  constexpr double inv_l = 1.0 / (double)L;
+  fft512_inv(a, slots + (c.warp() + 1) * SLOT, TW2(), TW32(), c.lane());
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    acc[0][m] = a[m].x * inv_l;
+    acc[1][m] = a[m].y * inv_l;
+  }
+  FTF(c, 8);
 }
 
 // acc = (M + sg K) PV for the owner rows (PV complete and visible; one group barrier inside)
 __device__ __forceinline__ void apply_pv(Ctx& c, double (&acc)[NOWN][8], double sg) {
   FT_MARK(c);
-  col_pass_apply(c);
+  col_pass_apply<false>(c);
   FT(c, 0);
   gsync(c.sy);
   FT(c, 1);
+  FTF(c, 5);
   row_pass_apply(c, acc, sg);
   double wv[NOWN][8];
   RM_OWN_FOR { wv[p][m] = __ldcg(c.WV() + own_e(c, p, m)); }
   RM_OWN_FOR { acc[p][m] = own_valid(c, p, m) ? fma(sg, wv[p][m], acc[p][m]) : 0.0; }
   FT(c, 2);
+  FTF(c, 9);
+}
+
+// The PCG loop's apply: acc = (M + sg K) PV for the owner rows and the group's p.Ap = PV . acc.  The column
+// owners sum the y-part's share of the dot product inside the column pass, so ONE group reduction delivers
+// p.Ap and is the barrier that publishes WV to the row owners.
+__device__ __forceinline__ double apply_pv_dot(Ctx& c, double (&acc)[NOWN][8], double sg) {
+  FT_MARK(c);
+  const double dcol = col_pass_apply<true>(c);
+  FT(c, 0);
+  FTF(c, 5);
+  row_pass_apply(c, acc, sg);
+  double part[1] = {sg * dcol};
+  {
+    double pv[NOWN][8];
+    RM_OWN_FOR { pv[p][m] = __ldcg(c.PV() + own_e(c, p, m)); }  // zero outside the grid
+    RM_OWN_FOR { part[0] = fma(pv[p][m], acc[p][m], part[0]); }
+  }
+  FT(c, 2);
+  double pap[1];
+  creduce<1>(c, part, pap);
+  FT(c, 3);
+  double wv[NOWN][8];
+  RM_OWN_FOR { wv[p][m] = __ldcg(c.WV() + own_e(c, p, m)); }
+  RM_OWN_FOR { acc[p][m] = own_valid(c, p, m) ? fma(sg, wv[p][m], acc[p][m]) : 0.0; }
+  FTF(c, 9);
+  return pap[0];
 }
 
 // refresh this CTA's 1/d(s) cache when s changed (once per sweep on uniform levels)
@@ -573,22 +669,28 @@ __device__ __forceinline__ void dinv_refresh(Ctx& c, double s) {
   }
 }
 
-// z = P(s)^-1 r = (Sy x Sx) diag(1/d(s)) (Sy x Sx) r for the owner rows (two group barriers)
+// z = P(s)^-1 r = (Sy x Sx) diag(1/d(s)) (Sy x Sx) r for the owner rows, in two halves around ONE group reduction.
 // The DST stages run as FP32 FFTs (FP32 intermediates SR / WV, FP32 1/d): P^-1 only steers the iteration --
 // every stop is decided on the FP64 true residual -- and FP32 keeps it within ~1e-7 of the FP64 operator.
-__device__ __forceinline__ void precond(Ctx& c, const double (&r)[NOWN][8], double (&z)[NOWN][8], double s) {
+//
+// precond_front: row DSTs of r, group barrier, column DST -> 1/d(s) -> column DST into WV.  The column owners hold
+// the full 2-D sine spectrum rhat = S r at that point, so r.z = r^T P^-1 r = sum rhat^2 / d is summed there
+// (FP64 accumulation of the FP32 spectrum); the group reduction that publishes WV to the row owners delivers
+// red = {sum of part0 over the group (the caller's r.r share), r.z}.
+__device__ __forceinline__ void precond_front(Ctx& c, const double (&r)[NOWN][8], double s, double part0,
+                                              double (&red)[2]) {
+  static_assert(PPW == 1, "one packed pair per warp");
   float2* slots = SLOTSF();
   FT_MARK(c);
   dinv_refresh(c, s);
-#pragma unroll 1
-  for (int h = 0; h < PPW; ++h) {  // SR[own rows] = Sx r (x-frequency along the row), pairs q = warp + WARPS h
+  {  // SR[own rows] = Sx r (x-frequency along the row), pair q = warp
     float2 a[16];
 #pragma unroll
-    for (int m = 0; m < 8; ++m) a[m] = make_float2((float)r[2 * h][m], (float)r[2 * h + 1][m]);
-    dst_fwd(a, slots + (c.warp() + WARPS * h) * SLOTF, TW2F(), TW32F(), c.lane(), HALF_CF);
+    for (int m = 0; m < 8; ++m) a[m] = make_float2((float)r[0][m], (float)r[1][m]);
+    dst_fwd(a, slots + c.warp() * SLOTF, TW2F(), TW32F(), c.lane(), HALF_CF);
     if ((c.lane() & 1) == 0) {
-      float* sa = c.SRf() + own_j(c, 2 * h) * NP - 1;
-      float* sb = c.SRf() + own_j(c, 2 * h + 1) * NP - 1;
+      float* sa = c.SRf() + own_j(c, 0) * NP - 1;
+      float* sb = c.SRf() + own_j(c, 1) * NP - 1;
 #pragma unroll
       for (int rr = 0; rr < 16; ++rr) {
         const int k = klay(c.lane(), rr);
@@ -602,16 +704,28 @@ __device__ __forceinline__ void precond(Ctx& c, const double (&r)[NOWN][8], doub
   FT(c, 5);
   gsync(c.sy);
   FT(c, 6);
+  double rz = 0.0;
   {  // column pass: WV[:, own columns] = Sy diag(1/d) Sy SR
-    for (int idx = c.tid(); idx < NP * H; idx += THREADS) {
-      const int j = idx / H, q = idx % H;
-      const float* row = c.SRf() + j * NP + c.C0();
-      slots[(q + 1) * SLOTF + j] = make_float2(__ldcg(row + q), __ldcg(row + q + H));
+    constexpr int NIT = NP * H / THREADS;
+    {
+      float2 v[NIT];
+#pragma unroll
+      for (int it = 0; it < NIT; ++it) {
+        const int idx = c.tid() + it * THREADS;
+        const int j = idx / H, q = idx % H;
+        const float* row = c.SRf() + j * NP + c.C0();
+        v[it] = make_float2(__ldcg(row + q), __ldcg(row + q + H));
+      }
+#pragma unroll
+      for (int it = 0; it < NIT; ++it) {
+        const int idx = c.tid() + it * THREADS;
+        const int j = idx / H, q = idx % H;
+        slots[(q + 1) * SLOTF + j] = v[it];
+      }
     }
     __syncthreads();
-#pragma unroll 1
-    for (int h = 0; h < PPW; ++h) {
-      const int q = c.warp() + WARPS * h;
+    {
+      const int q = c.warp();
       float2* sl = slots + (q + 1) * SLOTF;
       float2 a[16];
 #pragma unroll
@@ -621,7 +735,9 @@ __device__ __forceinline__ void precond(Ctx& c, const double (&r)[NOWN][8], doub
 #pragma unroll
       for (int rr = 0; rr < 16; ++rr) {
         const float2 d = __ldcg(di + rr * 32);
-        a[rr] = make_float2(a[rr].x * d.x, a[rr].y * d.y);
+        const float2 t = make_float2(a[rr].x * d.x, a[rr].y * d.y);
+        rz = fma((double)a[rr].x, (double)t.x, fma((double)a[rr].y, (double)t.y, rz));
+        a[rr] = t;
       }
       dst_inv(a, sl, TW2F(), TW32F(), c.lane(), HALF_CF);
       __syncwarp();
@@ -629,7 +745,9 @@ __device__ __forceinline__ void precond(Ctx& c, const double (&r)[NOWN][8], doub
       for (int m = 0; m < 8; ++m) sl[c.lane() + 32 * m] = a[m];
     }
     __syncthreads();
-    for (int idx = c.tid(); idx < NP * H; idx += THREADS) {
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+      const int idx = c.tid() + it * THREADS;
       const int j = idx / H, q = idx % H;
       const float2 t = slots[(q + 1) * SLOTF + j];
       c.WVf()[j * NP + c.C0() + q] = t.x;
@@ -637,29 +755,34 @@ __device__ __forceinline__ void precond(Ctx& c, const double (&r)[NOWN][8], doub
     }
   }
   FT(c, 7);
-  gsync(c.sy);
+  // the k-layout spectrum carries every frequency twice (k and its odd mirror L - k, same 1/d)
+  double part[2] = {part0, 0.5 * rz};
+  creduce<2>(c, part, red);
   FT(c, 8);
-#pragma unroll 1
-  for (int h = 0; h < PPW; ++h) {  // z[own rows] = Sx WV[own rows]
-    float2 a[16];
-    const float* wa = c.WVf() + own_j(c, 2 * h) * NP;
-    const float* wb = c.WVf() + own_j(c, 2 * h + 1) * NP;
+}
+
+// precond_back: z[own rows] = Sx WV[own rows] (after precond_front's reduction)
+__device__ __forceinline__ void precond_back(Ctx& c, double (&z)[NOWN][8]) {
+  float2* slots = SLOTSF();
+  FT_MARK(c);
+  float2 a[16];
+  const float* wa = c.WVf() + own_j(c, 0) * NP;
+  const float* wb = c.WVf() + own_j(c, 1) * NP;
 #pragma unroll
-    for (int rr = 0; rr < 16; ++rr) {
-      const int k = klay(c.lane(), rr);
-      float2 w = make_float2(0.f, 0.f);
-      if (k >= 1 && k <= 255)
-        w = make_float2(__ldcg(wa + k - 1), __ldcg(wb + k - 1));
-      else if (k >= 257)
-        w = make_float2(-__ldcg(wa + 511 - k), -__ldcg(wb + 511 - k));
-      a[rr] = w;
-    }
-    dst_inv(a, slots + (c.warp() + WARPS * h) * SLOTF, TW2F(), TW32F(), c.lane(), HALF_CF);
+  for (int rr = 0; rr < 16; ++rr) {
+    const int k = klay(c.lane(), rr);
+    float2 w = make_float2(0.f, 0.f);
+    if (k >= 1 && k <= 255)
+      w = make_float2(__ldcg(wa + k - 1), __ldcg(wb + k - 1));
+    else if (k >= 257)
+      w = make_float2(-__ldcg(wa + 511 - k), -__ldcg(wb + 511 - k));
+    a[rr] = w;
+  }
+  dst_inv(a, slots + c.warp() * SLOTF, TW2F(), TW32F(), c.lane(), HALF_CF);
 #pragma unroll
-    for (int m = 0; m < 8; ++m) {
-      z[2 * h][m] = own_valid(c, 2 * h, m) ? (double)a[m].x : 0.0;
-      z[2 * h + 1][m] = own_valid(c, 2 * h + 1, m) ? (double)a[m].y : 0.0;
-    }
+  for (int m = 0; m < 8; ++m) {
+    z[0][m] = own_valid(c, 0, m) ? (double)a[m].x : 0.0;
+    z[1][m] = own_valid(c, 1, m) ? (double)a[m].y : 0.0;
   }
   FT(c, 9);
 }
@@ -668,28 +791,30 @@ __device__ __forceinline__ void put_pv(Ctx& c, const double (&v)[NOWN][8]) {
   RM_OWN_FOR { c.PV()[own_e(c, p, m)] = v[p][m]; }
 }
 
-// p = z (PRE) or r into PV after the reduction of r.z (every CTA is then past its PV reads); returns r.z
+// p = z (PRE) or r into PV (every CTA is past its PV reads: the reduction of r.z is a group barrier); returns r.z
 template <bool PRE>
 __device__ __forceinline__ double start_direction(Ctx& c, double s, int64_t& npc) {
   double r0[NOWN][8], z[NOWN][8];
   RM_OWN_FOR { r0[p][m] = __ldcg(c.RV() + own_e(c, p, m)); }
-  double pr[1] = {0.0};
+  double rz;
   if constexpr (PRE) {
-    precond(c, r0, z, s);
+    double red[2];
+    precond_front(c, r0, s, 0.0, red);
     ++npc;
-    RM_OWN_FOR { r0[p][m] = __ldcg(c.RV() + own_e(c, p, m)); }  // (not kept live across the transforms)
-    RM_OWN_FOR { pr[0] += r0[p][m] * z[p][m]; }
+    rz = red[1];
+    precond_back(c, z);
   } else {
+    double pr[1] = {0.0}, o[1];
     RM_OWN_FOR {
       z[p][m] = r0[p][m];
       pr[0] += r0[p][m] * r0[p][m];
     }
+    creduce<1>(c, pr, o);
+    rz = o[0];
   }
-  double o[1];
-  creduce<1>(c, pr, o);
   put_pv(c, z);
   gsync(c.sy);
-  return o[0];
+  return rz;
 }
 
 }  // namespace fft
@@ -915,9 +1040,10 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
       if (W_.x0_mode == 3) {
         // preconditioner probe: x = P^-1 b
         if constexpr (PRE) {
-          double r0[NOWN][8], z[NOWN][8];
+          double r0[NOWN][8], z[NOWN][8], red[2];
           RM_OWN_FOR { r0[p][m] = __ldcg(c.RV() + own_e(c, p, m)); }
-          precond(c, r0, z, s);
+          precond_front(c, r0, s, 0.0, red);
+          precond_back(c, z);
           ++npc;
           RM_OWN_FOR { c.XV()[own_e(c, p, m)] = z[p][m]; }
         }
@@ -935,53 +1061,37 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
           break;
         }
         double ap[NOWN][8];
-        apply_pv(c, ap, s);
+        const double pap = apply_pv_dot(c, ap, s);  // one group reduction: p.Ap, and WV published
         ++nmv;
-        double p1[1] = {0.0};
-        {
-          double pv[NOWN][8];
-          RM_OWN_FOR { pv[p][m] = __ldcg(c.PV() + own_e(c, p, m)); }
-          RM_OWN_FOR { p1[0] += pv[p][m] * ap[p][m]; }
-        }
-        double pap[1];
-        FT_MARK(c);
-        creduce<1>(c, p1, pap);
-        FT(c, 3);
-        if (!isfinite(pap[0]) || pap[0] <= 0.0) {
+        if (!isfinite(pap) || pap <= 0.0) {
           fail = RM_CG_BREAKDOWN;
           its = k;
           break;
         }
-        alpha = rz / pap[0];
-        double rn[NOWN][8];
-        {
-          double rv[NOWN][8];
-          RM_OWN_FOR { rv[p][m] = __ldcg(c.RV() + own_e(c, p, m)); }
-          RM_OWN_FOR {
-            rn[p][m] = rv[p][m] - alpha * ap[p][m];
-            c.RV()[own_e(c, p, m)] = rn[p][m];
-          }
-        }
+        alpha = rz / pap;
         double red2[2];
-        double z[NOWN][8];
         {
-          double part2[2] = {0.0, 0.0};
-          if constexpr (PRE) {
-            RM_OWN_FOR { part2[0] += rn[p][m] * rn[p][m]; }
-            precond(c, rn, z, s);
-            ++npc;
-            RM_OWN_FOR { rn[p][m] = __ldcg(c.RV() + own_e(c, p, m)); }  // (not kept live across the transforms)
-            RM_OWN_FOR { part2[1] += rn[p][m] * z[p][m]; }
-          } else {
+          double rn[NOWN][8];
+          double rr = 0.0;
+          {
+            double rv[NOWN][8];
+            RM_OWN_FOR { rv[p][m] = __ldcg(c.RV() + own_e(c, p, m)); }
             RM_OWN_FOR {
-              z[p][m] = rn[p][m];
-              part2[0] += rn[p][m] * rn[p][m];
+              rn[p][m] = rv[p][m] - alpha * ap[p][m];
+              c.RV()[own_e(c, p, m)] = rn[p][m];
+              rr += rn[p][m] * rn[p][m];
             }
-            part2[1] = part2[0];
           }
-          FT_MARK(c);
-          creduce<2>(c, part2, red2);
-          FT(c, 10);
+          if constexpr (PRE) {
+            precond_front(c, rn, s, rr, red2);  // one group reduction: r.r and r.z, and the column DSTs published
+            ++npc;
+          } else {
+            double part1[1] = {rr}, o1[1];
+            FT_MARK(c);
+            creduce<1>(c, part1, o1);
+            FT(c, 10);
+            red2[0] = red2[1] = o1[0];
+          }
         }
         res = sqrt(red2[0]);
         if (!isfinite(res)) {
@@ -1039,6 +1149,13 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
         }
         const double beta = red2[1] / rz;
         rz = red2[1];
+        double z[NOWN][8];
+        if constexpr (PRE) {
+          precond_back(c, z);
+        } else {
+          RM_OWN_FOR { z[p][m] = __ldcg(c.RV() + own_e(c, p, m)); }
+        }
+        FT_MARK(c);
         // x += alpha p, p = z + beta p (every CTA finished reading PV: the reductions were group barriers)
         {
           double xo[NOWN][8], pv[NOWN][8];
