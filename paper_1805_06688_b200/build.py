@@ -21,7 +21,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIBNAME = "libriesz_mgrit_b200.so"
 SOURCES = ["rm_kernels.cu", "rm_big.cu", "rm_fft.cu", "rm_capi.cu"]
-HEADERS = ["rm_device.cuh", "rm_kernels.h"]
+HEADERS = ["rm_device.cuh", "rm_kernels.h", "rm_tc.cuh"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

@@ -13,6 +13,7 @@
 
 #include "riesz_mgrit_b200.h"
 #include "rm_kernels.h"
+#include "rm_tc.cuh"
 
 namespace {
 
@@ -73,6 +74,7 @@ struct rm_grid {
   double* d_fscratch = nullptr;
   double* d_dmT = nullptr;
   double* d_dkT = nullptr;
+  uint16_t* d_dstc = nullptr;  // FP16 DST-I matrix in the tcgen05 canonical layout (tensor-core preconditioner)
 };
 
 extern "C" {
@@ -233,6 +235,7 @@ int rm_grid_destroy(rm_grid* g) {
   cudaFree(g->d_fscratch);
   cudaFree(g->d_dmT);
   cudaFree(g->d_dkT);
+  cudaFree(g->d_dstc);
   delete g;
   return RM_OK;
 }
@@ -333,7 +336,12 @@ int rm_sweep_run(rm_grid* g, const rm_sweep* sw, void* stream) {
     a.gbuf = g->d_gbuf;
     a.sw = *sw;
     a.sw.lp_matvec = 0;
-    if (a.sw.precond) a.sw.precond = 1;  // FP64 throughout (the DST stages are FFTs)
+    // precond 1 ('tau64'): DST stages as FP32 FFTs; precond 2 ('tau', 'tau16'): on the tensor cores (FP16
+    // operands, FP32 accumulation; RM_FFT_TC=0 falls back to the FFT stages)
+    if (a.sw.precond == 2 && (!g->d_dstc || (getenv("RM_FFT_TC") && !atoi(getenv("RM_FFT_TC"))))) a.sw.precond = 1;
+    a.dstc = g->d_dstc;
+    a.lp_dmin = g->lp_dmin;
+    a.lp_kmin = g->lp_kmin;
     a.nx = g->nx;
     a.ny = g->ny;
     a.cm = g->cm;
@@ -463,6 +471,19 @@ int rm_grid_set_tau(rm_grid* g, const double* dm, const double* dk) {
       return cuda_fail(e, "rm_grid_set_tau");
     RM_CUDA(cudaMemcpy(g->d_dmT, mt.data(), n * sizeof(double), cudaMemcpyHostToDevice), "rm_grid_set_tau");
     RM_CUDA(cudaMemcpy(g->d_dkT, kt.data(), n * sizeof(double), cudaMemcpyHostToDevice), "rm_grid_set_tau");
+    // tensor-core preconditioner: the orthonormal DST-I matrix of order nx (= ny), zero-padded to 256, FP16,
+    // row-major (each CTA moves it into tensor memory once per launch)
+    std::vector<uint16_t> hc((size_t)rm::tc::NS * rm::tc::NS, 0);
+    const int nn = g->nx;
+    const double c = sqrt(2.0 / (nn + 1));
+    for (int a = 0; a < nn; ++a)
+      for (int b = 0; b < nn; ++b) {
+        const double v = c * sin(M_PI * (double)((a + 1) * (b + 1) % (2 * (nn + 1))) / (double)(nn + 1));
+        hc[(size_t)a * rm::tc::NS + b] = __half_as_ushort(__float2half_rn((float)v));
+      }
+    if (!g->d_dstc && (e = cudaMalloc(&g->d_dstc, hc.size() * sizeof(uint16_t))) != cudaSuccess)
+      return cuda_fail(e, "rm_grid_set_tau");
+    RM_CUDA(cudaMemcpy(g->d_dstc, hc.data(), hc.size() * sizeof(uint16_t), cudaMemcpyHostToDevice), "rm_grid_set_tau");
   }
   g->lp_dmin = dm[0];
   g->lp_kmin = dk[0];

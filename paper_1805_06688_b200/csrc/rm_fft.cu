@@ -34,6 +34,7 @@
 #include "riesz_mgrit_b200.h"
 #include "rm_device.cuh"
 #include "rm_kernels.h"
+#include "rm_tc.cuh"
 
 namespace rm {
 namespace fft {
@@ -56,8 +57,13 @@ constexpr size_t VEC = (size_t)NP * NP;
 constexpr size_t DIV = (size_t)H * 16 * 32 * 2;  // per-CTA 1/d(s) cache (doubles)
 constexpr int SLOTF = 1089;            // float2 per slot in the FP32 (preconditioner) passes: odd -> conflict-free
 static_assert(SLOTF * 8 <= SLOT * 16, "FP32 slots overlay the FP64 ones");
-constexpr size_t SMEM = sizeof(double2) * ((size_t)NSLOT * SLOT + L + 16 + 3 * L) + sizeof(double) * (4 * 32) +
-                        sizeof(float2) * (L + 16) + 64;
+constexpr size_t SMEM_FFT = sizeof(double2) * ((size_t)NSLOT * SLOT + L + 16 + 3 * L) + sizeof(double) * (4 * 32) +
+                            sizeof(float2) * (L + 16);
+// tensor-core preconditioner (PRE == 2, rm_tc.cuh): the strip operand, the mbarriers and the tensor-memory base
+// address follow the FFT tables (the DST matrix itself lives in tensor memory)
+constexpr size_t OFF_TCB = (SMEM_FFT + 127) / 128 * 128;
+constexpr size_t OFF_TCBAR = OFF_TCB + tc::B_BYTES;
+constexpr size_t SMEM = OFF_TCBAR + 64;
 static_assert(SMEM <= 227 * 1024, "shared memory budget");
 
 // complex arithmetic on double2 / float2 (the preconditioner's DSTs run in FP32, see precond)
@@ -356,6 +362,9 @@ struct Ctx {
   double di_s;         // s of the cached DI (NaN: none)
   Sync sy;
   int buf;
+  // tensor-core preconditioner state (PRE == 2; uniform over the CTA)
+  uint32_t tmem;        // tensor-memory base (512 columns: the DST matrix in [0, 256), accumulator from 256)
+  unsigned ph_mma;      // phase of the MMA-completion mbarrier
   __device__ __forceinline__ int tid() const { return threadIdx.x; }
   __device__ __forceinline__ int lane() const { return threadIdx.x & 31; }
   __device__ __forceinline__ int warp() const { return threadIdx.x >> 5; }
@@ -376,7 +385,7 @@ struct Ctx {
 };
 
 __device__ __forceinline__ double2* smem2() {
-  extern __shared__ __align__(16) double2 fft_smem[];
+  extern __shared__ __align__(128) double2 fft_smem[];
   return fft_smem;
 }
 __device__ __forceinline__ double2* SLOTS() { return smem2(); }
@@ -623,6 +632,7 @@ __device__ __forceinline__ void apply_pv(Ctx& c, double (&acc)[NOWN][8], double 
 // The PCG loop's apply: acc = (M + sg K) PV for the owner rows and the group's p.Ap = PV . acc.  The column
 // owners sum the y-part's share of the dot product inside the column pass, so ONE group reduction delivers
 // p.Ap and is the barrier that publishes WV to the row owners.
+template <int PRE>
 __device__ __forceinline__ double apply_pv_dot(Ctx& c, double (&acc)[NOWN][8], double sg) {
   FT_MARK(c);
   const double dcol = col_pass_apply<true>(c);
@@ -787,17 +797,189 @@ __device__ __forceinline__ void precond_back(Ctx& c, double (&z)[NOWN][8]) {
   FT(c, 9);
 }
 
+// ---- tensor-core tau preconditioner (PRE == 2) -------------------------------------------------------------
+// The four sine-transform stages as tcgen05 GEMMs (rm_tc.cuh): per CTA D[256][32] = S[256][256] X^T, S the FP16
+// DST-I matrix RESIDENT IN TENSOR MEMORY for the whole kernel (loaded once per launch), X a 32-row strip converted
+// to FP16 in shared memory, FP32 accumulation in tensor memory.  Intermediates cross the group in FP16,
+// transposed so that the next stage's strip operand is contiguous along its contraction index: SRh[kx][j]
+// (x-frequency major), WVh[j][kx].
+// Scaling: r is scaled by a power of two that maps the previous residual norm into [256, 512) -- the orthonormal
+// transforms preserve the 2-norm, so no entry exceeds it; conversions saturate instead of overflowing should the
+// norm grow more than 128-fold in one step -- and 1/d(s) is normalised by its upper bound 1/(min dm + s min dk).
+__device__ __forceinline__ __half* TC_B() {
+  return reinterpret_cast<__half*>(reinterpret_cast<unsigned char*>(smem2()) + OFF_TCB);
+}
+__device__ __forceinline__ uint64_t* TC_BARS() {
+  return reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(smem2()) + OFF_TCBAR);
+}
+__device__ __forceinline__ uint32_t* TC_TMEM_SLOT() { return reinterpret_cast<uint32_t*>(TC_BARS() + 2); }
+__device__ __forceinline__ __half* SRh(const Ctx& c) { return reinterpret_cast<__half*>(c.SR()); }
+__device__ __forceinline__ __half* WVh(const Ctx& c) { return reinterpret_cast<__half*>(c.WV()); }
+__device__ __forceinline__ float* DItc(const Ctx& c) { return reinterpret_cast<float*>(c.DI()); }
+
+__device__ __forceinline__ unsigned short f2h_sat(float x) {
+  unsigned short h;
+  asm("cvt.rn.satfinite.f16.f32 %0, %1;" : "=h"(h) : "f"(x));
+  return h;
+}
+
+// the strip operand is written: run the stage's 32 MMAs and wait for the accumulator
+__device__ __forceinline__ void tc_stage_mma(Ctx& c) {
+  tc::fence_async_smem();
+  tc::tc_fence_before();
+  __syncthreads();
+  if ((c.warp() & 3) == 0 && c.lane() == 0) {  // four issuers: M tile x K half each (rm_tc.cuh)
+    tc::tc_fence_after();
+    tc::issue_dst_mma_ts_part(TC_B(), c.tmem, c.warp() >> 2);
+    tc::tc_commit(TC_BARS() + 1);
+  }
+  tc::mbar_wait(TC_BARS() + 1, c.ph_mma);
+  c.ph_mma ^= 1;
+  tc::tc_fence_after();
+}
+
+// this warp's share of the accumulator: rows (lanes) 128 t + 32 q + lane, strip columns 16 h .. 16 h + 15
+__device__ __forceinline__ void tc_read(const Ctx& c, float (&v)[16], int& row, int& col0) {
+  const int q = c.warp() & 3, t = (c.warp() >> 2) & 1, h = c.warp() >> 3;
+  float w[16];  // the two K halves were accumulated separately
+  tc::tmem_ld16(c.tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(tc::TMEM_D_COL + tc::NB * (2 * t) + 16 * h), v);
+  tc::tmem_ld16(c.tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(tc::TMEM_D_COL + tc::NB * (2 * t + 1) + 16 * h), w);
+#pragma unroll
+  for (int e = 0; e < 16; ++e) v[e] += w[e];
+  row = 128 * t + 32 * q + c.lane();
+  col0 = 16 * h;
+}
+
+__device__ __forceinline__ void tc_store16h(__half* dst, const float (&v)[16]) {
+  uint32_t w[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) w[i] = (uint32_t)f2h_sat(v[2 * i]) | ((uint32_t)f2h_sat(v[2 * i + 1]) << 16);
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+  d4[0] = make_uint4(w[0], w[1], w[2], w[3]);
+  d4[1] = make_uint4(w[4], w[5], w[6], w[7]);
+}
+
+// strip operand = 32 consecutive rows of a [256][256] FP16 array (each row contiguous along the contraction index)
+__device__ __forceinline__ void tc_load_strip(const Ctx& c, const __half* rows) {
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const int ch = c.tid() + it * THREADS;  // 16-byte chunk: row n, contraction indices 8 jc .. 8 jc + 7
+    const int n = ch >> 5, jc = ch & 31;
+    const uint4 val = __ldcg(reinterpret_cast<const uint4*>(rows + n * NP + jc * 8));
+    *reinterpret_cast<uint4*>(TC_B() + tc::b_index(n, jc * 8)) = val;
+  }
+}
+
+// (1 / d(s)) / bound for this CTA's x-frequencies, [y-frequency l][32 x-frequencies], FP32
+__device__ __forceinline__ void dinv_refresh_tc(Ctx& c, double s) {
+  if (s == c.di_s) return;
+  c.di_s = s;
+  const double num = c.P->lp_dmin + s * c.P->lp_kmin;
+  for (int idx = c.tid(); idx < NP * tc::NB; idx += THREADS) {
+    const int kk = idx >> 8, l = idx & 255;
+    const int ca = c.C0() + kk;
+    float w = 0.f;
+    if (l < NX && ca < NX) w = (float)(num / (__ldg(c.P->dmT + ca * NX + l) + s * __ldg(c.P->dkT + ca * NX + l)));
+    DItc(c)[l * tc::NB + kk] = w;
+  }
+  __syncthreads();  // (read back below by other threads of this CTA; global memory, CTA scope)
+}
+
+// red = {group sum of part0, r.z}; nrm: a recent 2-norm of r (sets the power-of-two scaling)
+__device__ __forceinline__ void precond_front_tc(Ctx& c, const double (&r)[NOWN][8], double s, double nrm, double part0,
+                                                 double (&red)[2]) {
+  FT_MARK(c);
+  dinv_refresh_tc(c, s);
+  const double sc1 = (nrm > 0.0 && isfinite(nrm)) ? scalbn(1.0, 8 - ilogb(nrm)) : 1.0;
+  {  // stage 1: SRh[kx][own rows] = Sx r
+#pragma unroll
+    for (int p = 0; p < NOWN; ++p)
+#pragma unroll
+      for (int m = 0; m < 8; ++m)
+        reinterpret_cast<unsigned short*>(TC_B())[tc::b_index(c.warp() + H * p, c.lane() + 32 * m)] =
+            f2h_sat((float)(r[p][m] * sc1));
+    tc_stage_mma(c);
+    float v[16];
+    int k, j0;
+    tc_read(c, v, k, j0);
+    tc_store16h(SRh(c) + k * NP + c.R0() + j0, v);
+  }
+  FT(c, 5);
+  gsync(c.sy);
+  FT(c, 6);
+  double rz = 0.0;
+  {  // stage 2: Sy along the rows of SRh (own x-frequencies), 1/d, stage 3: Sy again, WVh[j][own x-frequencies]
+    tc_load_strip(c, SRh(c) + c.C0() * NP);
+    tc_stage_mma(c);
+    float v[16];
+    int l, k0;
+    tc_read(c, v, l, k0);
+    const float4* di = reinterpret_cast<const float4*>(DItc(c) + l * tc::NB + k0);
+#pragma unroll
+    for (int g4 = 0; g4 < 4; ++g4) {
+      const float4 d = __ldcg(di + g4);
+      const float dd[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float t = v[4 * g4 + e] * dd[e];
+        rz = fma((double)v[4 * g4 + e], (double)t, rz);
+        v[4 * g4 + e] = t;
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 16; ++e) reinterpret_cast<unsigned short*>(TC_B())[tc::b_index(k0 + e, l)] = f2h_sat(v[e]);
+    tc_stage_mma(c);
+    int j;
+    tc_read(c, v, j, k0);
+    tc_store16h(WVh(c) + j * NP + c.C0() + k0, v);
+  }
+  FT(c, 7);
+  const double bound = 1.0 / (c.P->lp_dmin + s * c.P->lp_kmin);
+  double part[2] = {part0, rz * bound / (sc1 * sc1)};
+  creduce<2>(c, part, red);
+  FT(c, 8);
+}
+
+// z[own rows] = Sx WVh[own rows], unscaled
+__device__ __forceinline__ void precond_back_tc(Ctx& c, double (&z)[NOWN][8], double s, double nrm) {
+  FT_MARK(c);
+  const double sc1 = (nrm > 0.0 && isfinite(nrm)) ? scalbn(1.0, 8 - ilogb(nrm)) : 1.0;
+  const double unscale = 1.0 / ((c.P->lp_dmin + s * c.P->lp_kmin) * sc1);
+  tc_load_strip(c, WVh(c) + c.R0() * NP);
+  tc_stage_mma(c);
+  float v[16];
+  int i, n0;
+  tc_read(c, v, i, n0);
+  float* zs = reinterpret_cast<float*>(smem2());  // [32 strip rows][256] in the (idle) FFT slots
+#pragma unroll
+  for (int e = 0; e < 16; ++e) zs[(n0 + e) * NP + i] = v[e];
+  __syncthreads();
+#pragma unroll
+  for (int p = 0; p < NOWN; ++p)
+#pragma unroll
+    for (int m = 0; m < 8; ++m)
+      z[p][m] = own_valid(c, p, m) ? (double)zs[(c.warp() + H * p) * NP + c.lane() + 32 * m] * unscale : 0.0;
+  FT(c, 9);
+}
+
+
 __device__ __forceinline__ void put_pv(Ctx& c, const double (&v)[NOWN][8]) {
   RM_OWN_FOR { c.PV()[own_e(c, p, m)] = v[p][m]; }
 }
 
 // p = z (PRE) or r into PV (every CTA is past its PV reads: the reduction of r.z is a group barrier); returns r.z
-template <bool PRE>
-__device__ __forceinline__ double start_direction(Ctx& c, double s, int64_t& npc) {
+template <int PRE>
+__device__ __forceinline__ double start_direction(Ctx& c, double s, double nrm, int64_t& npc) {
   double r0[NOWN][8], z[NOWN][8];
   RM_OWN_FOR { r0[p][m] = __ldcg(c.RV() + own_e(c, p, m)); }
   double rz;
-  if constexpr (PRE) {
+  if constexpr (PRE == 2) {
+    double red[2];
+    precond_front_tc(c, r0, s, nrm, 0.0, red);
+    ++npc;
+    rz = red[1];
+    precond_back_tc(c, z, s, nrm);
+  } else if constexpr (PRE == 1) {
     double red[2];
     precond_front(c, r0, s, 0.0, red);
     ++npc;
@@ -819,7 +1001,7 @@ __device__ __forceinline__ double start_direction(Ctx& c, double s, int64_t& npc
 
 }  // namespace fft
 
-template <bool PRE>
+template <int PRE>  // 0: plain CG, 1: tau preconditioner by FP32 FFTs, 2: tau preconditioner on the tensor cores
 __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid_constant__ ChainArgs P) {
   using namespace fft;
   Ctx c;
@@ -832,6 +1014,23 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
   c.sy.sched = reinterpret_cast<int*>(c.sy.gred + 8 * G);
   c.sy.epoch = 0;
   c.buf = 0;
+  c.tmem = 0;
+  c.ph_mma = 0;
+  if constexpr (PRE == 2) {
+    if (tid == 0) {
+      tc::mbar_init(TC_BARS() + 1, 4);  // four MMA issuers commit to it
+      tc::fence_mbar_init();
+    }
+    if (tid < 32) tc::tmem_alloc(TC_TMEM_SLOT(), tc::TMEM_COLS_RESIDENT);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    c.tmem = *TC_TMEM_SLOT();
+    // the DST matrix moves into tensor memory once per launch and stays there
+    tc::load_matrix_tmem(c.tmem, reinterpret_cast<const __half*>(P.dstc), tid >> 5, tid & 31);
+    tc::tc_fence_before();
+    __syncthreads();
+  }
   {
     double2* tw2 = const_cast<double2*>(TW2());    // tw2[q * 32 + t] = W512^{q t}
     double2* tw32 = const_cast<double2*>(TW32());  // W32^r = W512^{16 r}
@@ -1042,14 +1241,19 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
         if constexpr (PRE) {
           double r0[NOWN][8], z[NOWN][8], red[2];
           RM_OWN_FOR { r0[p][m] = __ldcg(c.RV() + own_e(c, p, m)); }
-          precond_front(c, r0, s, 0.0, red);
-          precond_back(c, z);
+          if constexpr (PRE == 2) {
+            precond_front_tc(c, r0, s, res, 0.0, red);
+            precond_back_tc(c, z, s, res);
+          } else {
+            precond_front(c, r0, s, 0.0, red);
+            precond_back(c, z);
+          }
           ++npc;
           RM_OWN_FOR { c.XV()[own_e(c, p, m)] = z[p][m]; }
         }
         done = true;
       }
-      if (!done) rz = start_direction<PRE>(c, s, npc);
+      if (!done) rz = start_direction<PRE>(c, s, res, npc);
 
       // PCG (krylov.py:57-86 with the tau preconditioner); x += alpha p is folded into the next direction
       // update (or the acceptance check), which reads p anyway
@@ -1061,7 +1265,7 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
           break;
         }
         double ap[NOWN][8];
-        const double pap = apply_pv_dot(c, ap, s);  // one group reduction: p.Ap, and WV published
+        const double pap = apply_pv_dot<PRE>(c, ap, s);  // one group reduction: p.Ap, and WV published
         ++nmv;
         if (!isfinite(pap) || pap <= 0.0) {
           fail = RM_CG_BREAKDOWN;
@@ -1069,6 +1273,7 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
           break;
         }
         alpha = rz / pap;
+        const double res_prev = res;
         double red2[2];
         {
           double rn[NOWN][8];
@@ -1082,7 +1287,10 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
               rr += rn[p][m] * rn[p][m];
             }
           }
-          if constexpr (PRE) {
+          if constexpr (PRE == 2) {
+            precond_front_tc(c, rn, s, res_prev, rr, red2);  // (res: the previous residual norm sets the FP16 scaling)
+            ++npc;
+          } else if constexpr (PRE == 1) {
             precond_front(c, rn, s, rr, red2);  // one group reduction: r.r and r.z, and the column DSTs published
             ++npc;
           } else {
@@ -1144,13 +1352,15 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
             done = true;
             break;
           }
-          rz = start_direction<PRE>(c, s, npc);
+          rz = start_direction<PRE>(c, s, res, npc);
           continue;
         }
         const double beta = red2[1] / rz;
         rz = red2[1];
         double z[NOWN][8];
-        if constexpr (PRE) {
+        if constexpr (PRE == 2) {
+          precond_back_tc(c, z, s, res_prev);
+        } else if constexpr (PRE == 1) {
           precond_back(c, z);
         } else {
           RM_OWN_FOR { z[p][m] = __ldcg(c.RV() + own_e(c, p, m)); }
@@ -1233,6 +1443,11 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
       gsync(c.sy);
     }
   }
+  if constexpr (PRE == 2) {
+    tc::tc_fence_before();
+    __syncthreads();
+    if (tid < 32) tc::tmem_free(c.tmem, tc::TMEM_COLS_RESIDENT);
+  }
 }
 
 #undef RM_OWN_FOR
@@ -1293,7 +1508,7 @@ static cudaError_t fft_prepare(const void* kern) {
 }
 
 cudaError_t fft_max_chains(int* out) {
-  auto kern = chain_fft_kernel<true>;
+  auto kern = chain_fft_kernel<1>;
   cudaError_t err = fft_prepare((const void*)kern);
   if (err != cudaSuccess) return err;
   int per_sm = 0, dev = 0, sms = 0;
@@ -1306,7 +1521,8 @@ cudaError_t fft_max_chains(int* out) {
 }
 
 cudaError_t launch_fft(const ChainArgs& a, int max_chains, cudaStream_t st) {
-  auto kern = a.sw.precond ? chain_fft_kernel<true> : chain_fft_kernel<false>;
+  if (a.sw.precond == 2 && !a.dstc) return cudaErrorInvalidValue;
+  auto kern = a.sw.precond == 2 ? chain_fft_kernel<2> : a.sw.precond ? chain_fft_kernel<1> : chain_fft_kernel<0>;
   cudaError_t err = fft_prepare((const void*)kern);
   if (err != cudaSuccess) return err;
   if (!a.gbar || !a.gbuf || !a.fscratch || !a.fsym) return cudaErrorInvalidValue;

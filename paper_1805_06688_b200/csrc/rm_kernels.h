@@ -34,6 +34,7 @@ struct ChainArgs {
   double* fscratch;        // per-chain vectors (fft_scratch_doubles_per_chain each)
   const double* dmT;       // tau diagonals transposed, [nx][ny]
   const double* dkT;
+  const uint16_t* dstc;    // FP16 DST-I matrix, order 256, row-major (tensor-core preconditioner, rm_tc.cuh)
 };
 
 struct ApplyArgs {
