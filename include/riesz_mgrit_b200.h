@@ -138,8 +138,10 @@ typedef struct rm_sweep {
   unsigned long long* d_counters;
   int group;   /* CTAs per chain (cluster size); 0 = library choice */
   int precond; /* 0: plain CG (the reference algorithm); 1: tau-preconditioned CG (needs
-                  rm_grid_set_tau), DST stages in FP64; 2: the same preconditioner with its DST stages
-                  on FP16 tensor cores (scaled, FP32 accumulation; square grids, others run 1);
+                  rm_grid_set_tau), DST stages in FP64 (255^2 FFT kernel: FP32 FFTs); 2: the same
+                  preconditioner with its DST stages on FP16 tensor cores (scaled, FP32 accumulation;
+                  square grids, others run 1; 255^2 FFT kernel: tcgen05.mma GEMMs with the DST matrix
+                  resident in tensor memory, RM_FFT_TC=0 falls back to 1);
                   all stop on ||b - A x|| <= rel_tol ||b|| in FP64 */
   /* optional second starting guess x0' = guess_n - G_n (G_n only when d_gadd): the solve starts
      from whichever of x0, x0' has the smaller initial residual (e.g. the iterate value this step

@@ -76,7 +76,7 @@ def build(force: bool = False, verbose: bool = False, timing: bool = False) -> s
     extra += [f"-D{d}" for d in os.environ.get("RM_DEFINES", "").split(",") if d]
     cache = os.environ.get("RM_OBJ_CACHE")  # developer option: keep objects, recompile stale sources only
     if cache:
-        objdir = os.path.join(cache, "timing" if timing else "plain")
+        objdir = os.path.join(cache, "_".join(["timing" if timing else "plain"] + [e[2:] for e in extra[1 if timing else 0:]]))
         os.makedirs(objdir, exist_ok=True)
     else:
         objdir = tempfile.mkdtemp(prefix="rm_build_", dir=LIBDIR)  # private: concurrent builds do not collide

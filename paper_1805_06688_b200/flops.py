@@ -60,5 +60,12 @@ def fpc_fft(nx: int, ny: int) -> float:
     return 2.0 * ((ny + 1) // 2 + (nx + 1) // 2) * fft_flops(L) + 2.0 * nx * ny
 
 
+def fpc_tc(nx: int, ny: int) -> float:
+    """One tau-preconditioner application on the 5th-generation tensor cores as executed (csrc/rm_tc.cuh): four
+    DST-I stages, each a dense 256 x 256 GEMM against every row / column of the padded 256 x 256 grid."""
+    n = 256 if max(nx, ny) <= 255 else 2 * (max(nx, ny) + 1)
+    return 4.0 * 2.0 * n * n * n
+
+
 # legacy mma.sync m16n8k16 FP16 -> FP32 on B200, measured with tools/lowp_peak.cu (profiles/r01_lowp_peak.txt)
 FP16_MMA_SYNC_PEAK_TFLOPS = 555.0
