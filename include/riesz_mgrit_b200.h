@@ -226,6 +226,16 @@ RM_API int rm_correct(int ndof, int nc, int m, double* d_u, int64_t u_stride, co
 RM_API int rm_diff_sqnorm(int64_t n, const double* d_a, const double* d_b, double* d_out, void* stream);
 
 /*
+ * Vector algebra of cg_solve for an ARBITRARY operator (krylov.py:44: `op.apply` or a bare callable; the
+ * reference's tests pass dense SPD matrices): d_out[0] = a . b in a fixed summation order, and
+ * out = alpha x + beta y (out may alias x or y).  The package's own step operator never takes this route: its
+ * CG runs fused inside the chain kernels (rm_sweep_run).
+ */
+RM_API int rm_vec_dot(int64_t n, const double* d_a, const double* d_b, double* d_out, void* stream);
+RM_API int rm_vec_axpby(int64_t n, double alpha, const double* d_x, double beta, const double* d_y, double* d_out,
+                        void* stream);
+
+/*
  * numpy PCG64 uniform doubles, bit-identical to
  * np.random.default_rng(seed).random(): draw number (start + i) is written to
  * d_out[(i / row) * out_stride + i % row] for i < count.  state/inc are the

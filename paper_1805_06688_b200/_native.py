@@ -73,6 +73,8 @@ EXPORTS = {
     "rm_correct": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
                              C.c_void_p]),
     "rm_diff_sqnorm": (C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "rm_vec_dot": (C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "rm_vec_axpby": (C.c_int, [C.c_int64, C.c_double, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]),
     "rm_pcg64_uniform": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int64, C.c_int64,
                                    C.c_int64, C.c_void_p, C.c_int64, C.c_void_p]),
 }

@@ -548,6 +548,19 @@ int rm_diff_sqnorm(int64_t n, const double* d_a, const double* d_b, double* d_ou
   return RM_OK;
 }
 
+int rm_vec_dot(int64_t n, const double* d_a, const double* d_b, double* d_out, void* stream) {
+  if (n < 0 || !d_a || !d_b || !d_out) return fail(RM_EINVAL, "rm_vec_dot: bad argument");
+  RM_CUDA(rm::launch_vec_dot(n, d_a, d_b, d_out, (cudaStream_t)stream), "rm_vec_dot");
+  return RM_OK;
+}
+
+int rm_vec_axpby(int64_t n, double alpha, const double* d_x, double beta, const double* d_y, double* d_out,
+                 void* stream) {
+  if (n < 0 || !d_x || !d_y || !d_out) return fail(RM_EINVAL, "rm_vec_axpby: bad argument");
+  RM_CUDA(rm::launch_vec_axpby(n, alpha, d_x, beta, d_y, d_out, (cudaStream_t)stream), "rm_vec_axpby");
+  return RM_OK;
+}
+
 int rm_pcg64_uniform(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t start,
                      int64_t count, int64_t row, double* d_out, int64_t out_stride, void* stream) {
   if (count < 0 || start < 0 || row < 1 || !d_out) return fail(RM_EINVAL, "rm_pcg64_uniform: bad argument");

@@ -1269,6 +1269,27 @@ __global__ void diff_sqnorm_kernel(int64_t n, const double* a, const double* b, 
   }
 }
 
+// dot product a . b into out[0]: one CTA, fixed summation order (generic-operator CG, krylov.py:57-66)
+__global__ void vec_dot_kernel(int64_t n, const double* a, const double* b, double* out) {
+  __shared__ double sm[32];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s = fma(a[i], b[i], s);
+  s = warp_allsum(s);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double x = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
+    x = warp_allsum(x);
+    if (threadIdx.x == 0) out[0] = x;
+  }
+}
+
+// out = alpha x + beta y (out may alias x or y)
+__global__ void vec_axpby_kernel(int64_t n, double alpha, const double* x, double beta, const double* y, double* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = alpha * x[i] + beta * y[i];
+}
+
 #endif
 
 // ----------------------------------------------------------------------------
@@ -1423,6 +1444,20 @@ cudaError_t launch_correct(int ndof, int nc, int m, double* u, int64_t us, const
 
 cudaError_t launch_diff_sqnorm(int64_t n, const double* a, const double* b, double* out, cudaStream_t st) {
   diff_sqnorm_kernel<<<1, 1024, 0, st>>>(n, a, b, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_vec_dot(int64_t n, const double* a, const double* b, double* out, cudaStream_t st) {
+  vec_dot_kernel<<<1, 1024, 0, st>>>(n, a, b, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_vec_axpby(int64_t n, double alpha, const double* x, double beta, const double* y, double* out,
+                             cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  const int threads = 256;
+  const int64_t blocks = (n + threads - 1) / threads;
+  vec_axpby_kernel<<<(unsigned)(blocks < 148 * 8 ? blocks : 148 * 8), threads, 0, st>>>(n, alpha, x, beta, y, out);
   return cudaGetLastError();
 }
 

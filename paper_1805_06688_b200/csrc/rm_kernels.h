@@ -77,5 +77,8 @@ cudaError_t fft_max_chains(int* out);
 cudaError_t launch_fft(const ChainArgs& a, int max_chains, cudaStream_t st);
 bool fft_symbols(const double* tab, int np, int gl, double* out_klayout);
 cudaError_t launch_diff_sqnorm(int64_t n, const double* a, const double* b, double* out, cudaStream_t st);
+cudaError_t launch_vec_dot(int64_t n, const double* a, const double* b, double* out, cudaStream_t st);
+cudaError_t launch_vec_axpby(int64_t n, double alpha, const double* x, double beta, const double* y, double* out,
+                             cudaStream_t st);
 
 }  // namespace rm

@@ -132,10 +132,85 @@ def test_cg_budget_failure_raises():
     assert err.value.iterations == 2
 
 
-def test_cg_rejects_explicit_side():
+# cg_solve with an arbitrary operator (krylov.py:44; the reference's tests/test_krylov.py cases): same algorithm,
+# vectors and reductions on the device (rm_vec_dot / rm_vec_axpby), the operator called once per iteration
+class _SpdOperator:
+    def __init__(self, dense):
+        self.dense = dense
+
+    def apply(self, v):
+        return self.dense @ v
+
+
+def _random_spd(n, rng, cond=100.0):
+    Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    return Q @ np.diag(np.geomspace(1.0, cond, n)) @ Q.T
+
+
+def test_generic_cg_matches_direct_solve_and_oracle():
+    rng = np.random.default_rng(12345)
+    A = _random_spd(40, rng)
+    b = rng.standard_normal(40)
+    x, iters = cg_solve(_SpdOperator(A), b, opts=CgOptions(rel_tol=1e-12))
+    assert x == pytest.approx(np.linalg.solve(A, b), abs=1e-8)
+    from oracle import riesz_oracle as O
+
+    xo, io = O.cg(lambda v: A @ v, b, rel_tol=1e-12)
+    assert iters == io and np.linalg.norm(x - xo) <= 1e-10 * np.linalg.norm(xo)
+
+
+def test_generic_cg_accepts_plain_callable_and_device_operator():
+    rng = np.random.default_rng(3)
+    A = _random_spd(10, rng)
+    b = rng.standard_normal(10)
+    x, _ = cg_solve(lambda v: A @ v, b, opts=CgOptions(rel_tol=1e-12))
+    assert A @ x == pytest.approx(b, abs=1e-9)
+    At = torch.from_numpy(A).cuda()
+
+    class Dev:
+        accepts_device = True
+
+        def apply(self, v):
+            return At @ v
+
+    xd, _ = cg_solve(Dev(), torch.from_numpy(b).cuda(), opts=CgOptions(rel_tol=1e-12))
+    assert xd.is_cuda and xd.cpu().numpy() == pytest.approx(x, abs=1e-9)
+
+
+def test_generic_cg_warm_start_zero_rhs_and_tolerance():
+    rng = np.random.default_rng(5)
+    A = _random_spd(20, rng)
+    b = rng.standard_normal(20)
+    x_exact = np.linalg.solve(A, b)
+    x, iters = cg_solve(_SpdOperator(A), b, x0=x_exact)
+    assert iters == 0 and x == pytest.approx(x_exact)
+    x, iters = cg_solve(_SpdOperator(A), np.zeros(20))
+    assert iters == 0 and x == pytest.approx(np.zeros(20))
+    A = _random_spd(30, rng, cond=1e4)
+    b = rng.standard_normal(30)
+    x, _ = cg_solve(_SpdOperator(A), b, opts=CgOptions(rel_tol=1e-10))
+    assert np.linalg.norm(b - A @ x) <= 1e-10 * np.linalg.norm(b) * 10
+
+
+def test_generic_cg_failures():
+    from paper_1805_06688_b200.krylov import CgFailure
+
+    with pytest.raises(CgFailure):
+        cg_solve(_SpdOperator(np.diag([1.0, -1.0, 2.0, -2.0])), np.ones(4))
+    rng = np.random.default_rng(7)
+    A = _random_spd(50, rng, cond=1e8)
+    with pytest.raises(CgFailure) as err:
+        cg_solve(_SpdOperator(A), rng.standard_normal(50), opts=CgOptions(rel_tol=1e-14, max_iter=2))
+    assert err.value.iterations == 2
+
+
+def test_generic_cg_runs_the_package_operators():
+    """The explicit-side operator (and any BttbOperator) goes through the generic route with its device apply."""
     disc = Discretization(man_spec(8, 4))
-    with pytest.raises(TypeError):
-        cg_solve(disc.combined(0.1, -1), np.ones(disc.ndof))
+    op = disc.combined(1e-3, -1)  # M - s K at a small step: SPD
+    b = np.random.default_rng(2).standard_normal(disc.ndof)
+    x, iters = cg_solve(op, b, opts=CgOptions(rel_tol=1e-12))
+    assert iters > 0 and np.linalg.norm(op.apply(x) - b) <= 1e-11 * np.linalg.norm(b)
 
 
 # ----------------------------------------------------------------------------- stepper

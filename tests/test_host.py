@@ -171,7 +171,7 @@ def header_functions():
 def test_library_exports_every_header_symbol():
     lib = _native.lib()
     names = header_functions()
-    assert len(names) == 15
+    assert len(names) == 17
     for n in names:
         assert hasattr(lib, n), n
     assert set(names) == set(_native.EXPORTS)
