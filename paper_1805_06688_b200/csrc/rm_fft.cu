@@ -351,10 +351,29 @@ __device__ __forceinline__ void greduce(double (&part)[NV], double* wred, Sync& 
 #else
 #define FTF(c, slot)
 #endif
+#if defined(RM_TIMING) && defined(RM_TIMING_SOLVE)
+// solve-level slots (replace the others: -DRM_TIMING,RM_TIMING_SOLVE): 0 step prologue (right-hand side, initial
+// residual, second guess), 1 first direction, 2 PCG iterations, 3 acceptance (true residual), 4 epilogue
+#undef FT
+#define FT(c, slot)
+#undef FTF
+#define FTF(c, slot)
+#define ST_MARK(c) (c).s_mark = clock64()
+#define ST(c, slot)                                                            \
+  do {                                                                         \
+    const long long t_now_ = clock64();                                        \
+    if (blockIdx.x == 0 && threadIdx.x == 0) (c).P->timing[slot] += t_now_ - (c).s_mark; \
+    (c).s_mark = t_now_;                                                       \
+  } while (0)
+#else
+#define ST_MARK(c)
+#define ST(c, slot)
+#endif
 
 struct Ctx {
 #ifdef RM_TIMING
   long long t_mark;
+  long long s_mark;
 #endif
   double* base;        // this chain's vectors
   const ChainArgs* P;
@@ -1074,6 +1093,7 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
     bool chain_ok = false;
     double s_prev = 0.0;
     for (int n = n0; n <= n1; ++n) {
+      ST_MARK(c);
       const double s = 0.5 * W_.d_dt[n - 1];
       const double fs = W_.d_f ? (W_.d_fscale ? W_.d_fscale[n] : 1.0) : 0.0;
       const double* Fn = W_.d_f ? W_.d_f + (int64_t)n * W_.f_stride : nullptr;
@@ -1091,8 +1111,10 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
         put_pv(c, v);
         gsync(c.sy);
       }
+      ST(c, 5);
       double mv[NOWN][8];  // M v of the step input (explicit sides without an apply, x0 = v)
       if (rhs_free || rhs_ain) mass_own(c, mv);
+      ST(c, 6);
       if (rhs_free) {
         const double* Hn = W_.d_hg + (int64_t)(n - 1) * W_.hg_stride;
         const double q = s / s_prev;
@@ -1179,8 +1201,10 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
           }
         }
       }
+      ST(c, 7);
       double tot[2];
       creduce<2>(c, part, tot);
+      ST(c, 8);
       const double bnorm = sqrt(tot[0]);
       const double target = bnorm > 0.0 ? W_.rel_tol * bnorm : W_.rel_tol;
       if (W_.d_guess && W_.x0_mode < 3 && sqrt(tot[1]) > target) {
@@ -1253,7 +1277,9 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
         }
         done = true;
       }
+      ST(c, 0);
       if (!done) rz = start_direction<PRE>(c, s, res, npc);
+      ST(c, 1);
 
       // PCG (krylov.py:57-86 with the tau preconditioner); x += alpha p is folded into the next direction
       // update (or the acceptance check), which reads p anyway
@@ -1308,6 +1334,7 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
           break;
         }
         if (res <= target) {
+          ST(c, 2);
           // x += alpha p, then acceptance on the true residual (krylov.py:71-83); every CTA is past its PV
           // reads (the reductions above were group barriers)
           double xv[NOWN][8];
@@ -1341,6 +1368,7 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
           creduce<1>(c, pt, tt);
           const double true_res = sqrt(tt[0]);
           RM_OWN_FOR { c.RV()[own_e(c, p, m)] = ax[p][m]; }
+          ST(c, 3);
           if (true_res <= fmax(target, 10.0 * res)) {
             its = k;
             done = true;
@@ -1383,6 +1411,7 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
         FT(c, 11);
       }
 
+      ST(c, 2);
       chain_ok = done && !fail && W_.x0_mode < 3;
       if (c.rank == 0 && tid == 0) {
         atomicAdd(W_.d_counters, 1ull);
@@ -1441,6 +1470,7 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
       }
       in_tile = next_in_tile;
       gsync(c.sy);
+      ST(c, 4);
     }
   }
   if constexpr (PRE == 2) {
