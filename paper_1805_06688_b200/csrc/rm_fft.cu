@@ -63,7 +63,9 @@ constexpr size_t SMEM_FFT = sizeof(double2) * ((size_t)NSLOT * SLOT + L + 16 + 3
 // address follow the FFT tables (the DST matrix itself lives in tensor memory)
 constexpr size_t OFF_TCB = (SMEM_FFT + 127) / 128 * 128;
 constexpr size_t OFF_TCBAR = OFF_TCB + tc::B_BYTES;
-constexpr size_t SMEM = OFF_TCBAR + 64;
+// two more spectrum slots: the row pass's halo pairs are transformed during the column pass's halo round
+constexpr size_t OFF_XSLOT = OFF_TCBAR + 64;
+constexpr size_t SMEM = OFF_XSLOT + 2 * sizeof(double2) * SLOT;
 static_assert(SMEM <= 227 * 1024, "shared memory budget");
 
 // complex arithmetic on double2 / float2 (the preconditioner's DSTs run in FP32, see precond)
@@ -408,6 +410,9 @@ __device__ __forceinline__ double2* smem2() {
   return fft_smem;
 }
 __device__ __forceinline__ double2* SLOTS() { return smem2(); }
+__device__ __forceinline__ double2* XSLOT(int which) {  // row-pass halo spectra: 0 = pair (R0-1, R0+15), 1 = (R0+16, R0+32)
+  return reinterpret_cast<double2*>(reinterpret_cast<unsigned char*>(smem2()) + OFF_XSLOT) + which * SLOT;
+}
 __device__ __forceinline__ const double2* TW2() { return smem2() + NSLOT * SLOT; }
 __device__ __forceinline__ const double2* TW32() { return smem2() + NSLOT * SLOT + L; }
 // stiffness spectra (k-layout): per direction d (0 = x, 1 = y) the diagonal block's (real: T1 is symmetric)
@@ -455,33 +460,56 @@ __device__ __forceinline__ void mass_own(const Ctx& c, double (&out)[NOWN][8]) {
   }
 }
 
-// forward FFTs of a pass's packed pairs: the two halo slots first (warps 0 and WARPS-1, which are the warps
-// whose output pair couples to them), then every warp its own pair (slot warp + 1), whose spectrum stays in
+// forward FFT of the warp's own pair (slot warp + 1): the spectrum is stored for the neighbours and stays in
 // registers for the combination; LOAD(s, a) fills a[0..8) with the pair of slot s (a[8..16) = 0: zero padding
 // known at compile time, so the first radix stage is pruned)
 template <class LOAD>
-__device__ __forceinline__ void forward_pairs(Ctx& c, double2 (&a)[16], LOAD load) {
-  double2* slots = SLOTS();
-  if (c.warp() == 0 || c.warp() == WARPS - 1) {
-    const int s = c.warp() == 0 ? 0 : NSLOT - 1;
-    load(s, a);
+__device__ __forceinline__ void own_forward(Ctx& c, double2 (&a)[16], LOAD load) {
+  const int s = c.warp() + 1;
+  load(s, a);
+#pragma unroll
+  for (int m = 8; m < 16; ++m) a[m] = make_double2(0.0, 0.0);
+  double2* sl = SLOTS() + s * SLOT;
+  fft512_fwd(a, sl, TW2(), TW32(), c.lane());
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) sl[r * 32 + c.lane()] = a[r];
+}
+
+// the row pass's pair of slot s (rows R0 + s - 1 and R0 + s - 1 + H) from PV
+__device__ __forceinline__ void load_row_pair(const Ctx& c, int s, double2 (&x)[16]) {
+  const int ja = c.R0() + s - 1, jb = c.R0() + s - 1 + H;
+  const double* ra = c.PV() + ja * NP + c.lane();
+  const double* rb = c.PV() + jb * NP + c.lane();
+  const bool va = ja >= 0, vb = jb < NP;
+#pragma unroll
+  for (int m = 0; m < 8; ++m) x[m] = make_double2(va ? __ldcg(ra + 32 * m) : 0.0, vb ? __ldcg(rb + 32 * m) : 0.0);
+}
+
+// The halo round of an apply: the two halo pairs of the column pass (warps 0 and WARPS-1: slots 0 and NSLOT-1,
+// staged columns) and, at the same time, the two halo pairs of the ROW pass (warps 1 and WARPS-2: rows R0-1 / R0+32
+// with their partners, straight from PV, into the extra slots), so that the row pass needs no halo round of its own.
+__device__ __forceinline__ void halo_forward(Ctx& c, double2 (&a)[16]) {
+  const int w = c.warp();
+  if (w < 2 || w >= WARPS - 2) {
+    const bool row = (w == 1 || w == WARPS - 2);
+    const bool hi = w >= WARPS - 2;
+    const int s = hi ? NSLOT - 1 : 0;
+    double2* sl = row ? XSLOT(hi) : SLOTS() + s * SLOT;
+    if (row) {
+      load_row_pair(c, s, a);
+    } else {
+#pragma unroll
+      for (int m = 0; m < 8; ++m) a[m] = sl[c.lane() + 32 * m];
+      __syncwarp();  // (the slot doubles as the transform's transpose scratch)
+    }
 #pragma unroll
     for (int m = 8; m < 16; ++m) a[m] = make_double2(0.0, 0.0);
-    double2* sl = slots + s * SLOT;
     fft512_fwd(a, sl, TW2(), TW32(), c.lane());
     __syncwarp();
 #pragma unroll
     for (int r = 0; r < 16; ++r) sl[r * 32 + c.lane()] = a[r];
   }
-  const int s = c.warp() + 1;
-  load(s, a);
-#pragma unroll
-  for (int m = 8; m < 16; ++m) a[m] = make_double2(0.0, 0.0);
-  double2* sl = slots + s * SLOT;
-  fft512_fwd(a, sl, TW2(), TW32(), c.lane());
-  __syncwarp();
-#pragma unroll
-  for (int r = 0; r < 16; ++r) sl[r * 32 + c.lane()] = a[r];
 }
 
 // y-direction pass of the stiffness: WV[:, own columns] = (1/L) sum_t IFFT(S_t FFT(PV columns i + 0/+1/-1)).
@@ -517,7 +545,8 @@ __device__ __forceinline__ double col_pass_apply(Ctx& c) {
   __syncthreads();
   FTF(c, 0);
   double2 a[16];  // own pair q = warp
-  forward_pairs(c, a, [&](int s, double2 (&x)[16]) {
+  halo_forward(c, a);
+  own_forward(c, a, [&](int s, double2 (&x)[16]) {
     const double2* sl = slots + s * SLOT;
 #pragma unroll
     for (int m = 0; m < 8; ++m) x[m] = sl[c.lane() + 32 * m];
@@ -588,15 +617,8 @@ __device__ __forceinline__ double col_pass_apply(Ctx& c) {
 // 6 + 2 cos(theta), 1 + e^{i theta}, 1 + e^{-i theta}, theta = 2 pi k / L (rm_device.cuh build_step_tables)
 __device__ __forceinline__ void row_pass_apply(Ctx& c, double (&acc)[NOWN][8], double sg) {
   double2* slots = SLOTS();
-  double2 a[16];  // own pair q = warp
-  forward_pairs(c, a, [&](int s, double2 (&x)[16]) {
-    const int ja = c.R0() + s - 1, jb = c.R0() + s - 1 + H;
-    const double* ra = c.PV() + ja * NP + c.lane();
-    const double* rb = c.PV() + jb * NP + c.lane();
-    const bool va = ja >= 0, vb = jb < NP;
-#pragma unroll
-    for (int m = 0; m < 8; ++m) x[m] = make_double2(va ? __ldcg(ra + 32 * m) : 0.0, vb ? __ldcg(rb + 32 * m) : 0.0);
-  });
+  double2 a[16];  // own pair q = warp (the halo pairs' spectra come from the column pass's halo round)
+  own_forward(c, a, [&](int s, double2 (&x)[16]) { load_row_pair(c, s, x); });
   __syncthreads();
   FTF(c, 6);
   {
@@ -604,8 +626,8 @@ __device__ __forceinline__ void row_pass_apply(Ctx& c, double (&acc)[NOWN][8], d
     const double sgn = (c.lane() & 1) ? -1.0 : 1.0;   // W512^{256 v}
     const double cm = c.P->cm;
     const double2* s0 = slots + (c.warp() + 1) * SLOT;
-    const double2* sp = s0 + SLOT;
-    const double2* sm = s0 - SLOT;
+    const double2* sp = c.warp() == WARPS - 1 ? XSLOT(1) : s0 + SLOT;
+    const double2* sm = c.warp() == 0 ? XSLOT(0) : s0 - SLOT;
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
       const int e = r * 32 + c.lane();
