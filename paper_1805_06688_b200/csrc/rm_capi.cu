@@ -335,10 +335,13 @@ int rm_sweep_run(rm_grid* g, const rm_sweep* sw, void* stream) {
     a.gbar = g->d_gbar;
     a.gbuf = g->d_gbuf;
     a.sw = *sw;
-    a.sw.lp_matvec = 0;
+    // lp_matvec (with precond 2): FP32-FFT in-iteration applies once |r| <= lp_thr |b| (RM_FFT_LP_THR, 0 = off)
+    a.lp_thr = 1e-6;
+    if (const char* t = getenv("RM_FFT_LP_THR")) a.lp_thr = atof(t);
     // precond 1 ('tau64'): DST stages as FP32 FFTs; precond 2 ('tau', 'tau16'): on the tensor cores (FP16
     // operands, FP32 accumulation; RM_FFT_TC=0 falls back to the FFT stages)
     if (a.sw.precond == 2 && (!g->d_dstc || (getenv("RM_FFT_TC") && !atoi(getenv("RM_FFT_TC"))))) a.sw.precond = 1;
+    if (a.sw.precond != 2) a.sw.lp_matvec = 0;
     a.dstc = g->d_dstc;
     a.lp_dmin = g->lp_dmin;
     a.lp_kmin = g->lp_kmin;

@@ -34,6 +34,7 @@ struct ChainArgs {
   double* fscratch;        // per-chain vectors (fft_scratch_doubles_per_chain each)
   const double* dmT;       // tau diagonals transposed, [nx][ny]
   const double* dkT;
+  double lp_thr;           // FFT kernel, lp_matvec: FP32 in-iteration applies once |r| <= lp_thr |b| (0: never)
   const uint16_t* dstc;    // FP16 DST-I matrix, order 256, row-major (tensor-core preconditioner, rm_tc.cuh)
 };
 

@@ -75,7 +75,7 @@ def main():
             print(f"  {tag:12s} launches={s['launches']:4d} chains={s['chains']:5d} ms={s['ms']:9.2f} "
                   f"solves={s['solves']:7d} cg/solve={s['cg'] / max(s['solves'], 1):7.1f} "
                   f"pc/solve={s['pc'] / max(s['solves'], 1):5.1f} "
-                  f"fp64mv/solve={s['mv'] / max(s['solves'], 1):5.1f} "
+                  f"fp64mv/solve={s['mv'] / max(s['solves'], 1):5.1f} mv16/solve={s['mv16'] / max(s['solves'], 1):5.2f} "
                   f"TF/s={((s['mv'] + s['mv16']) * F + s['pc'] * FP) / max(s['ms'], 1e-9) / 1e9:6.2f}")
         print("  residuals:", ["%.3e" % r for r in tr.residual_norms])
     if a.counts_json:
