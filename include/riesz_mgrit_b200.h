@@ -154,7 +154,9 @@ typedef struct rm_sweep {
   int64_t keep_stride;
   /* 1: inside the PCG iteration (precond 2), apply the operator to the search direction as a three-term
      split-FP16 tensor-core product (~2^-22 relative; rm_device.cuh Mx), every stopping decision still on
-     the FP64 true residual; grids 63^2 .. 127^2 (others ignore the flag).  0: FP64 throughout. */
+     the FP64 true residual; grids 63^2 .. 127^2.  255^2 (FFT kernel, precond 2): the in-iteration applies run
+     through FP32 FFTs once |r| <= 1e-6 |b| (RM_FFT_LP_THR), acceptance on the FP64 true residual as always.
+     Other grids ignore the flag.  0: FP64 throughout. */
   int lp_matvec;
   /* optional (explicit_rhs chains): rows n = (M + dt_n/2 K) G_n, dt_n = d_dt[n-1], of the G added in the
      epilogue (d_gadd; zero rows if none).  Inside a chain the next step's explicit side then follows from
