@@ -79,6 +79,31 @@ def test_fft_precond_tensor_core_matches_numpy():
         assert rel(got[k], ref[k]) <= 2e-3, (k, rel(got[k], ref[k]))
 
 
+def test_fft_relaxed_precision_applies():
+    """'tau' on the FFT kernel applies the operator through FP32 FFTs once |r| <= 1e-6 |b| (rm_sweep.lp_matvec with
+    precond 2), 'tau16' keeps every apply in FP64: same iteration count, both accepted on the FP64
+    true residual at 1e-12, and the FP32 applies are really used (counter slot 4)."""
+    case = make_case("cfg3", Nt=4)
+    spec = ProblemSpec(**case.problem_kwargs())
+    g = case.grid
+    rng = np.random.default_rng(7)
+    V = vectors(g, rng)[1:2]                       # a smooth state
+    out, its, lowp = {}, {}, {}
+    for pre in ("tau", "tau16"):
+        disc = Discretization(spec, cg_opts=CgOptions(rel_tol=1e-12, preconditioner=pre))
+        out[pre] = disc.propagate(1.0 / 16384, V)
+        its[pre] = int(disc.counters[1].item())
+        lowp[pre] = int(disc.counters[4].item())
+    assert its["tau"] == its["tau16"] and its["tau"] > 0
+    assert lowp["tau"] > 0 and lowp["tau16"] == 0
+    assert rel(out["tau"][0], out["tau16"][0]) <= 1e-11
+    ops = O.Operators(O.Grid(g.mx, g.my), case.kx, case.ky, case.beta, case.gamma)
+    b = ops.step_apply(1.0 / 16384, -1, V[0])
+    for pre in out:  # the FP64 true residual of the returned solution
+        r = b - ops.step_apply(1.0 / 16384, +1, out[pre][0])
+        assert np.linalg.norm(r) <= 1.5e-12 * np.linalg.norm(b), (pre, np.linalg.norm(r) / np.linalg.norm(b))
+
+
 def test_fft_solve_is_deterministic():
     """Same inputs, same bits: the group reductions are fixed-order and chain results do not depend on which CTA
     group picks a chain up (tools/determinism_check.py runs the long version)."""
