@@ -445,18 +445,31 @@ __device__ __forceinline__ void creduce(Ctx& c, double (&part)[NV], double (&out
 
 // M v of the owner rows from PV (7-point P1 mass; per step, not per iteration)
 __device__ __forceinline__ void mass_own(const Ctx& c, double (&out)[NOWN][8]) {
-  RM_OWN_FOR {
-    const int j = own_j(c, p), i = own_i(c, m);
-    const double* q = c.PV() + j * NP + i;
-    double s = 0.0;
-    if (own_valid(c, p, m)) {
-      const double up = __ldcg(q + NP), upr = __ldcg(q + NP + 1), ce = __ldcg(q), r = __ldcg(q + 1);
-      const double l = i > 0 ? __ldcg(q - 1) : 0.0;
-      const double dn = j > 0 ? __ldcg(q - NP) : 0.0;
-      const double dnl = (j > 0 && i > 0) ? __ldcg(q - NP - 1) : 0.0;
-      s = c.P->cm * (6.0 * ce + l + r + up + upr + dn + dnl);
+#pragma unroll
+  for (int p = 0; p < NOWN; ++p) {
+#pragma unroll
+    for (int m0 = 0; m0 < 8; m0 += 4) {  // (four elements' 28 loads in flight, then the arithmetic)
+      double up[4], upr[4], ce[4], r[4], l[4], dn[4], dnl[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int m = m0 + u;
+        const int j = own_j(c, p), i = own_i(c, m);
+        const double* q = c.PV() + j * NP + i;
+        const bool ok = own_valid(c, p, m);
+        up[u] = ok ? __ldcg(q + NP) : 0.0;
+        upr[u] = ok ? __ldcg(q + NP + 1) : 0.0;
+        ce[u] = ok ? __ldcg(q) : 0.0;
+        r[u] = ok ? __ldcg(q + 1) : 0.0;
+        l[u] = (ok && i > 0) ? __ldcg(q - 1) : 0.0;
+        dn[u] = (ok && j > 0) ? __ldcg(q - NP) : 0.0;
+        dnl[u] = (ok && j > 0 && i > 0) ? __ldcg(q - NP - 1) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        out[p][m0 + u] = own_valid(c, p, m0 + u)
+                             ? c.P->cm * (6.0 * ce[u] + l[u] + r[u] + up[u] + upr[u] + dn[u] + dnl[u])
+                             : 0.0;
     }
-    out[p][m] = s;
   }
 }
 
@@ -529,9 +542,14 @@ __device__ __forceinline__ void load_row_pair(const Ctx& c, int s, V (&x)[16]) {
   const double* ra = c.PV() + ja * NP + c.lane();
   const double* rb = c.PV() + jb * NP + c.lane();
   const bool va = ja >= 0, vb = jb < NP;
+  double da[8], db[8];  // (raw loads first, then the conversion)
 #pragma unroll
-  for (int m = 0; m < 8; ++m)
-    x[m] = Cx<V>::mk((R)(va ? __ldcg(ra + 32 * m) : 0.0), (R)(vb ? __ldcg(rb + 32 * m) : 0.0));
+  for (int m = 0; m < 8; ++m) {
+    da[m] = va ? __ldcg(ra + 32 * m) : 0.0;
+    db[m] = vb ? __ldcg(rb + 32 * m) : 0.0;
+  }
+#pragma unroll
+  for (int m = 0; m < 8; ++m) x[m] = Cx<V>::mk((R)da[m], (R)db[m]);
 }
 
 // The halo round of an apply: the two halo pairs of the column pass (warps 0 and WARPS-1: slots 0 and NSLOT-1,
@@ -576,29 +594,32 @@ __device__ __forceinline__ double col_pass_apply(Ctx& c) {
 #pragma unroll
     for (int k = 0; k < 6 * L / THREADS; ++k) SYMF()[c.tid() + k * THREADS] = (float)sym[c.tid() + k * THREADS];
   }
+  FTF(c, 10);
   {  // stage columns C0-1 .. C0+32: slot s = (column C0+s-1, column C0+s+15), natural row order; the loads of a
      // batch are issued before its first store
     constexpr int NIT = NP * NSLOT / THREADS, NB = 3;
     static_assert(NIT % NB == 0, "staging batches");
 #pragma unroll 1
     for (int it0 = 0; it0 < NIT; it0 += NB) {
-      V v[NB];
+      double va[NB], vb[NB];  // (raw loads first: a conversion between two loads would serialise their round trips)
 #pragma unroll
       for (int it = 0; it < NB; ++it) {
         const int idx = c.tid() + (it0 + it) * THREADS;
         const int j = idx / NSLOT, s = idx - j * NSLOT;
         const int ca = c.C0() + s - 1, cb = c.C0() + s + H - 1;
         const double* row = c.PV() + j * NP;
-        v[it] = Cx<V>::mk((R)(ca >= 0 ? __ldcg(row + ca) : 0.0), (R)(cb < NP ? __ldcg(row + cb) : 0.0));
+        va[it] = ca >= 0 ? __ldcg(row + ca) : 0.0;
+        vb[it] = cb < NP ? __ldcg(row + cb) : 0.0;
       }
 #pragma unroll
       for (int it = 0; it < NB; ++it) {
         const int idx = c.tid() + (it0 + it) * THREADS;
         const int j = idx / NSLOT, s = idx - j * NSLOT;
-        slots[s * ST + j] = v[it];
+        slots[s * ST + j] = Cx<V>::mk((R)va[it], (R)vb[it]);
       }
     }
   }
+  FTF(c, 11);
   __syncthreads();
   FTF(c, 0);
   V a[16];  // own pair q = warp
@@ -965,12 +986,18 @@ __device__ __forceinline__ void tc_store16h(__half* dst, const float (&v)[16]) {
 
 // strip operand = 32 consecutive rows of a [256][256] FP16 array (each row contiguous along the contraction index)
 __device__ __forceinline__ void tc_load_strip(const Ctx& c, const __half* rows) {
+  uint4 val[2];
 #pragma unroll
   for (int it = 0; it < 2; ++it) {
     const int ch = c.tid() + it * THREADS;  // 16-byte chunk: row n, contraction indices 8 jc .. 8 jc + 7
     const int n = ch >> 5, jc = ch & 31;
-    const uint4 val = __ldcg(reinterpret_cast<const uint4*>(rows + n * NP + jc * 8));
-    *reinterpret_cast<uint4*>(TC_B() + tc::b_index(n, jc * 8)) = val;
+    val[it] = __ldcg(reinterpret_cast<const uint4*>(rows + n * NP + jc * 8));
+  }
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const int ch = c.tid() + it * THREADS;
+    const int n = ch >> 5, jc = ch & 31;
+    *reinterpret_cast<uint4*>(TC_B() + tc::b_index(n, jc * 8)) = val[it];
   }
 }
 
@@ -1019,9 +1046,12 @@ __device__ __forceinline__ void precond_front_tc(Ctx& c, const double (&r)[NOWN]
     int l, k0;
     tc_read(c, v, l, k0);
     const float4* di = reinterpret_cast<const float4*>(DItc(c) + l * tc::NB + k0);
+    float4 dq[4];
+#pragma unroll
+    for (int g4 = 0; g4 < 4; ++g4) dq[g4] = __ldcg(di + g4);  // (all loads before the first use)
 #pragma unroll
     for (int g4 = 0; g4 < 4; ++g4) {
-      const float4 d = __ldcg(di + g4);
+      const float4 d = dq[g4];
       const float dd[4] = {d.x, d.y, d.z, d.w};
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -1210,10 +1240,12 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
           const bool ok = own_valid(c, p, m);
           bv[p][m] = __ldcg(c.BV() + e);
           rv[p][m] = __ldcg(c.RV() + e);
-          hv[p][m] = ok ? gsc(n - 1) * __ldcg(Hn + own_j(c, p) * nx + own_i(c, m)) : 0.0;
+          hv[p][m] = ok ? __ldcg(Hn + own_j(c, p) * nx + own_i(c, m)) : 0.0;  // (raw: arithmetic after the loads)
         }
+        const double gs1 = gsc(n - 1);
         RM_OWN_FOR {
-          acc[p][m] = own_valid(c, p, m) ? (1.0 + q) * mv[p][m] - q * (bv[p][m] - rv[p][m] + hv[p][m]) : 0.0;
+          acc[p][m] =
+              own_valid(c, p, m) ? (1.0 + q) * mv[p][m] - q * (bv[p][m] - rv[p][m] + gs1 * hv[p][m]) : 0.0;
         }
       } else if (rhs_ain) {
         const double* An = W_.d_ain + (int64_t)(n - 1) * W_.ain_stride;
@@ -1224,9 +1256,12 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
           const int gi = own_j(c, p) * nx + own_i(c, m);
           const bool ok = own_valid(c, p, m);
           av[p][m] = ok ? __ldcg(An + gi) : 0.0;
-          hv[p][m] = ok ? gsc(n - 1) * __ldcg(Hn + gi) : 0.0;
+          hv[p][m] = ok ? __ldcg(Hn + gi) : 0.0;
         }
-        RM_OWN_FOR { acc[p][m] = own_valid(c, p, m) ? (1.0 + q) * mv[p][m] - q * (av[p][m] + hv[p][m]) : 0.0; }
+        const double gs1 = gsc(n - 1);
+        RM_OWN_FOR {
+          acc[p][m] = own_valid(c, p, m) ? (1.0 + q) * mv[p][m] - q * (av[p][m] + gs1 * hv[p][m]) : 0.0;
+        }
       } else if (need_in) {
         apply_pv(c, acc, -s);  // (M - s K) v
         nmv = 1;
@@ -1297,14 +1332,17 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
         const double* gu = W_.d_guess + (int64_t)n * W_.guess_stride;
         const double* Gr = W_.d_gadd ? W_.d_gadd + (int64_t)n * W_.gadd_stride : nullptr;
         const double* Ax0 = W_.d_gax ? W_.d_gax + (int64_t)n * W_.gax_stride : nullptr;
-        auto guess_vec = [&](double (&g0)[NOWN][8]) {
+        auto guess_vec = [&](double (&g0)[NOWN][8]) {  // (all loads first, then the arithmetic)
+          double gr[NOWN][8];
           RM_OWN_FOR {
-            double v = 0.0;
-            if (own_valid(c, p, m)) {
-              const int gi = own_j(c, p) * nx + own_i(c, m);
-              v = Gr ? __ldcg(gu + gi) - gsc(n) * __ldcg(Gr + gi) : __ldcg(gu + gi);
-            }
-            g0[p][m] = v;
+            const bool ok = own_valid(c, p, m);
+            const int gi = own_j(c, p) * nx + own_i(c, m);
+            g0[p][m] = ok ? __ldcg(gu + gi) : 0.0;
+            gr[p][m] = (ok && Gr) ? __ldcg(Gr + gi) : 0.0;
+          }
+          if (Gr) {
+            const double gs0 = gsc(n);
+            RM_OWN_FOR { g0[p][m] = g0[p][m] - gs0 * gr[p][m]; }
           }
         };
         double ag[NOWN][8];
@@ -1320,10 +1358,14 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
           RM_OWN_FOR { ag[p][m] = own_valid(c, p, m) ? __ldcg(Ax0 + own_j(c, p) * nx + own_i(c, m)) : 0.0; }
         }
         double pg[1] = {0.0};
-        RM_OWN_FOR {
-          const double r = own_valid(c, p, m) ? __ldcg(c.BV() + own_e(c, p, m)) - ag[p][m] : 0.0;
-          ag[p][m] = r;
-          pg[0] += r * r;
+        {
+          double bq[NOWN][8];
+          RM_OWN_FOR { bq[p][m] = __ldcg(c.BV() + own_e(c, p, m)); }
+          RM_OWN_FOR {
+            const double r = own_valid(c, p, m) ? bq[p][m] - ag[p][m] : 0.0;
+            ag[p][m] = r;
+            pg[0] += r * r;
+          }
         }
         double rg[1];
         creduce<1>(c, pg, rg);
@@ -1538,11 +1580,12 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
       double py[1] = {0.0};
       {
         double xv[NOWN][8], gv[NOWN][8], sv[NOWN][8], bv[NOWN][8], rv[NOWN][8];
+        const double gsn = Gn ? gsc(n) : 0.0;
         RM_OWN_FOR {
           const bool ok = own_valid(c, p, m);
           const int e = own_e(c, p, m), gi = own_j(c, p) * nx + own_i(c, m);
           xv[p][m] = __ldcg(c.XV() + e);
-          gv[p][m] = (Gn && ok) ? gsc(n) * __ldcg(Gn + gi) : 0.0;
+          gv[p][m] = (Gn && ok) ? __ldcg(Gn + gi) : 0.0;  // (scaled below: arithmetic after the loads)
           sv[p][m] = (Sn && ok) ? __ldcg(Sn + gi) : 0.0;
           bv[p][m] = An ? __ldcg(c.BV() + e) : 0.0;
           rv[p][m] = An ? __ldcg(c.RV() + e) : 0.0;
@@ -1552,7 +1595,7 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
             const int gi = own_j(c, p) * nx + own_i(c, m);
             double y = xv[p][m];
             if (An) An[gi] = bv[p][m] - rv[p][m];  // A x = b - r (true residual)
-            if (Gn) y = gv[p][m] + y;
+            if (Gn) y = gsn * gv[p][m] + y;
             if (Kn) Kn[gi] = y;
             if (Sn) y = y - sv[p][m];
             if (On) On[gi] = y;

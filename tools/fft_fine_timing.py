@@ -7,7 +7,7 @@ import fft_phase_timing as base
 
 base.NAMES = ["col: stage from L2", "col: forward FFTs (18 on 16 warps)", "col: combine", "col: inverse FFTs",
               "col: store WV", "apply: group barrier", "row: load + forward FFTs", "row: combine",
-              "row: inverse FFTs", "row: add WV", "", "", "", "", "", ""]
+              "row: inverse FFTs", "row: add WV", "col: (FP32) symbol copies", "col: staging loads + stores", "", "", "", ""]
 
 if __name__ == "__main__":
     base.main()
