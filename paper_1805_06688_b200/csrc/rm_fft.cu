@@ -319,8 +319,11 @@ __device__ __forceinline__ void greduce(double (&part)[NV], double* wred, Sync& 
   }
   gsync(sy);
   // every warp sums the G tile partials with the same butterfly: identical in all CTAs
+  double g[NV];
 #pragma unroll
-  for (int v = 0; v < NV; ++v) out[v] = warp_allsum(lane < G ? __ldcg(sy.gred + (buf * 4 + v) * G + lane) : 0.0);
+  for (int v = 0; v < NV; ++v) g[v] = lane < G ? __ldcg(sy.gred + (buf * 4 + v) * G + lane) : 0.0;  // (loads first)
+#pragma unroll
+  for (int v = 0; v < NV; ++v) out[v] = warp_allsum(g[v]);
   buf ^= 1;
 }
 
@@ -1304,18 +1307,21 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
         const double* x0 = W_.x0_mode == 2 ? W_.d_x0 + (int64_t)n * W_.x0_stride : Fn;
         const double sc = W_.x0_mode == 2 ? 1.0 : fs;
         double v[NOWN][8];
-        RM_OWN_FOR { v[p][m] = own_valid(c, p, m) ? sc * __ldcg(x0 + own_j(c, p) * nx + own_i(c, m)) : 0.0; }
+        RM_OWN_FOR { v[p][m] = own_valid(c, p, m) ? __ldcg(x0 + own_j(c, p) * nx + own_i(c, m)) : 0.0; }
+        RM_OWN_FOR { v[p][m] = sc * v[p][m]; }
         put_pv(c, v);
         gsync(c.sy);
         apply_pv(c, acc, s);
         ++nmv;
         part[1] = 0.0;
+        double bq[NOWN][8];
+        RM_OWN_FOR { bq[p][m] = W_.x0_mode == 4 ? 0.0 : __ldcg(c.BV() + own_e(c, p, m)); }
         RM_OWN_FOR {
           const int e = own_e(c, p, m);
           if (W_.x0_mode == 4) {
             c.XV()[e] = acc[p][m];
           } else {
-            const double r = own_valid(c, p, m) ? __ldcg(c.BV() + e) - acc[p][m] : 0.0;
+            const double r = own_valid(c, p, m) ? bq[p][m] - acc[p][m] : 0.0;
             c.XV()[e] = v[p][m];
             c.RV()[e] = r;
             part[1] += r * r;
