@@ -245,6 +245,8 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": tts * 1e3, "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic (canonical seeded recipe)",
         "config": workload(case),
+        "solver": {"mgrit_iterations": counts.get("mgrit_iterations"), "cg_preconditioner": "none (reference CG)",
+                   "parallelism": f"host CPU, {threads} threads"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
                          "sample_wall_s": statistics.median(t_run), "extrapolated_tts_s": tts},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -513,9 +515,10 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (canonical seeded recipe, SURVEY.md §8d)",
-            "config": dict(workload(case), mgrit_iterations=iters, cg_preconditioner=args.precond,
-                           parallelism=(f"time slabs x{ws} (contiguous coarse intervals per rank, NCCL C-point "
-                                        f"exchange, pipelined coarsest level)" if ws > 1 else "single GPU")),
+            "config": workload(case),  # identical in both arms (the driver compares them)
+            "solver": {"mgrit_iterations": iters, "cg_preconditioner": args.precond,
+                       "parallelism": (f"time slabs x{ws} (slab-local level arrays, NCCL C-point exchange, coarse "
+                                       f"levels gathered on rank 0)" if ws > 1 else "single GPU")},
             "e2e": {"value": work / (e2e * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": len(e2e_ms)},
             "gpu_launches": launches // args.steps,
