@@ -289,7 +289,7 @@ def measured_peaks():
 
 def ncu_summary(fft: bool):
     """DRAM traffic per launch of the dominant kernel from the committed ncu capture summary (profiles/)."""
-    path = os.path.join(PROFILES, "r02b_ncu_fft_summary.json" if fft else "ncu_chain_summary.json")
+    path = os.path.join(PROFILES, "r02c_ncu_fft_summary.json" if fft else "ncu_chain_summary.json")
     if os.path.exists(path):
         with open(path) as f:
             return json.load(f)

@@ -36,6 +36,13 @@
 #include "rm_kernels.h"
 #include "rm_tc.cuh"
 
+#ifndef RM_STAGE_NB
+#define RM_STAGE_NB 3  // column-staging loads in flight per thread and batch (x2 values)
+#endif
+#ifndef RM_STORE_NB
+#define RM_STORE_NB 4  // column-store batch
+#endif
+
 namespace rm {
 namespace fft {
 
@@ -600,7 +607,7 @@ __device__ __forceinline__ double col_pass_apply(Ctx& c) {
   FTF(c, 10);
   {  // stage columns C0-1 .. C0+32: slot s = (column C0+s-1, column C0+s+15), natural row order; the loads of a
      // batch are issued before its first store
-    constexpr int NIT = NP * NSLOT / THREADS, NB = 3;
+    constexpr int NIT = NP * NSLOT / THREADS, NB = RM_STAGE_NB;
     static_assert(NIT % NB == 0, "staging batches");
 #pragma unroll 1
     for (int it0 = 0; it0 < NIT; it0 += NB) {
@@ -664,7 +671,7 @@ __device__ __forceinline__ double col_pass_apply(Ctx& c) {
   // store the 32 own columns, one row per half-warp step
   double dot = 0.0;
   {
-    constexpr int NIT = NP * H / THREADS, NB = 4;
+    constexpr int NIT = NP * H / THREADS, NB = RM_STORE_NB;
     static_assert(NIT % NB == 0, "store batches");
 #pragma unroll 1
     for (int it0 = 0; it0 < NIT; it0 += NB) {
