@@ -39,6 +39,9 @@
 #ifndef RM_STAGE_NB
 #define RM_STAGE_NB 3  // column-staging loads in flight per thread and batch (x2 values)
 #endif
+#ifndef RM_CNT_T
+#define RM_CNT_T int64_t  // per-solve iteration / apply counters
+#endif
 #ifndef RM_STORE_NB
 #define RM_STORE_NB 4  // column-store batch
 #endif
@@ -1113,7 +1116,7 @@ __device__ __forceinline__ void put_pv(Ctx& c, const double (&v)[NOWN][8]) {
 
 // p = z (PRE) or r into PV (every CTA is past its PV reads: the reduction of r.z is a group barrier); returns r.z
 template <int PRE>
-__device__ __forceinline__ double start_direction(Ctx& c, double s, double nrm, int64_t& npc) {
+__device__ __forceinline__ double start_direction(Ctx& c, double s, double nrm, RM_CNT_T& npc) {
   double r0[NOWN][8], z[NOWN][8];
   RM_OWN_FOR { r0[p][m] = __ldcg(c.RV() + own_e(c, p, m)); }
   double rz;
@@ -1197,7 +1200,8 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
   const rm_sweep& W_ = P.sw;
   constexpr int nx = NX;
   c.di_s = __longlong_as_double(0x7ff8000000000000ll);  // NaN: nothing cached
-  const int64_t max_iter = W_.max_iter > 0 ? W_.max_iter : 10 * (int64_t)NX * NX;
+  const RM_CNT_T max_iter =
+      (RM_CNT_T)(W_.max_iter > 0 ? (W_.max_iter < 2000000000 ? W_.max_iter : 2000000000) : 10 * (int64_t)NX * NX);
   const bool need_in = W_.explicit_rhs || W_.x0_mode == 1;
   const bool lowp_ok = W_.lp_matvec != 0 && P.lp_thr > 0.0;
   // G row scale (compressed G, rm_sweep.d_gscale): rows of d_gadd / d_hg are d_gscale[n] times the stored row
@@ -1227,7 +1231,7 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
                             W_.d_gadd != nullptr && W_.d_sub == nullptr;
       const bool rhs_ain = need_in && W_.explicit_rhs && !in_tile && n >= 2 && W_.d_ain != nullptr &&
                            W_.d_hg != nullptr && !rhs_free;
-      int64_t nmv = 0, npc = 0, nmv32 = 0;
+      RM_CNT_T nmv = 0, npc = 0, nmv32 = 0;
       double acc[NOWN][8];
       RM_OWN_FOR { acc[p][m] = 0.0; }
       if (need_in && !in_tile) {
@@ -1398,7 +1402,7 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
       }
       double res = sqrt(tot[1]);
       double rz = tot[1];
-      int64_t its = 0;
+      RM_CNT_T its = 0;
       int fail = 0;
       bool done = res <= target || W_.x0_mode == 4;
       if (W_.x0_mode == 3) {
@@ -1425,7 +1429,7 @@ __global__ void __launch_bounds__(fft::THREADS, 1) chain_fft_kernel(const __grid
       // PCG (krylov.py:57-86 with the tau preconditioner); x += alpha p is folded into the next direction
       // update (or the acceptance check), which reads p anyway
       double alpha = 0.0;
-      for (int64_t k = 1; !done; ++k) {
+      for (RM_CNT_T k = 1; !done; ++k) {
         if (k > max_iter) {
           fail = RM_CG_BUDGET;
           its = max_iter;
