@@ -78,3 +78,44 @@ def test_iteration_budget(pre):
     with pytest.raises(CgFailure) as err:
         cg_solve(disc.combined(0.5, +1), b, opts=CgOptions(rel_tol=1e-14, max_iter=2, preconditioner=pre))
     assert err.value.iterations == 2
+
+
+# ---- scalability proxy and spatial-solve overhead model (reference tests/test_acceptance.py:405-447, criterion 9; the
+# reference runs them with its dense 'direct' solver, here the CG paths of the device kernels) ----------------------
+def _proxy_spec(M, N):
+    c = manufactured(0.6, 0.7, 2.0, 0.5)
+    return ProblemSpec(SpatialGrid(M, M), uniform_temporal(1.0, N), c["kx"], c["ky"], c["beta"], c["gamma"],
+                       c["source"], c["initial"])
+
+
+@pytest.mark.parametrize("pre", PRECONDS)
+def test_iteration_count_stable_in_N(pre):
+    counts = []
+    for N in (256, 1024, 4096):
+        _, trace = solve(_proxy_spec(16, N), MgritOptions(m=4, halt_tol=1e-9, cg_rel_tol=1e-12, cg_preconditioner=pre))
+        assert trace.converged
+        counts.append(trace.iterations)
+    assert max(counts) - min(counts) <= 2, counts
+
+
+@pytest.mark.parametrize("pre", PRECONDS)
+def test_spatial_solve_overhead_model(pre):
+    """One multilevel cycle costs about (2m/(m-1) + 1) solves per coarse interval summed over the hierarchy, linear in N;
+    sequential stepping costs exactly N solves."""
+    m = 4
+    per_cycle = {}
+    for N in (512, 1024):
+        opts = MgritOptions(m=m, halt_tol=1e-9, cg_rel_tol=1e-12, skip_first_down=False, cg_preconditioner=pre)
+        _, trace = solve(_proxy_spec(8, N), opts)
+        per_cycle[N] = float(np.mean(np.diff(trace.spatial_solves)[1:]))
+        coarse_sum, n_l = 0, N
+        while n_l % m == 0 and n_l // m >= 2:
+            coarse_sum += n_l // m
+            n_l //= m
+        model = (2 * m / (m - 1) + 1) * coarse_sum
+        assert 0.25 <= model / per_cycle[N] <= 4.0, (per_cycle[N], model)
+    assert per_cycle[1024] / per_cycle[512] == pytest.approx(2.0, rel=0.25)
+    spec = _proxy_spec(8, 512)
+    disc = Discretization(spec, cg_opts=CgOptions(rel_tol=1e-12, preconditioner=pre))
+    sequential_solve(spec, disc)
+    assert disc.spatial_solves == 512
