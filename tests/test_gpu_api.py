@@ -1,0 +1,174 @@
+"""The reference's stepper and solve behaviours on the GPU path (reference tests/test_stepper.py, tests/test_mgrit.py
+TestSolve), with the oracle's dense operators as the independent check where the reference uses its dense 'direct'
+solver: argument validation, dense-solve parity of ``implicit_solve`` / ``propagate`` / ``step``, solve counters, load
+vectors, the space-time residual of the sequential solution and of a perturbed one, trace contents, seeds, and
+multilevel == two-level == sequential.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import manufactured
+from oracle import riesz_oracle as O
+from paper_1805_06688_b200.krylov import CgOptions
+from paper_1805_06688_b200.mesh import SpatialGrid, uniform_temporal
+from paper_1805_06688_b200.mgrit import MgritOptions, parareal_solve, solve
+from paper_1805_06688_b200.stepper import (Discretization, ProblemSpec, initial_vector, load_vector, sequential_solve,
+                                           spacetime_residual, step)
+
+pytestmark = pytest.mark.gpu
+PRECONDS = ["tau", "none"]
+
+
+def make(M=4, N=4, **over):
+    c = dict(manufactured(), **over)
+    return ProblemSpec(SpatialGrid(M, M), uniform_temporal(1.0, N), c["kx"], c["ky"], c["beta"], c["gamma"],
+                       c["source"], c["initial"]), c
+
+
+def dense_ops(spec):
+    return O.Operators(O.Grid(spec.grid.mx, spec.grid.my), spec.kx, spec.ky, spec.beta, spec.gamma)
+
+
+def host(a):
+    return a.cpu().numpy() if hasattr(a, "cpu") else np.asarray(a)
+
+
+# ---- ProblemSpec / Discretization (test_stepper.py:18-95) --------------------------------------------------------
+def test_problem_spec_validation():
+    c = manufactured()
+    grid, tmesh = SpatialGrid(4, 4), uniform_temporal(1.0, 4)
+    for beta in (0.5, 1.0, 0.3):
+        with pytest.raises(ValueError):
+            ProblemSpec(grid, tmesh, 1.0, 1.0, beta, 0.8, c["source"], c["initial"])
+    with pytest.raises(ValueError):
+        ProblemSpec(grid, tmesh, 0.0, 1.0, 0.8, 0.8, c["source"], c["initial"])
+    spec, _ = make()
+    with pytest.raises(ValueError):
+        Discretization(spec, solver="lu")
+    with pytest.raises(NotImplementedError):  # the dense Cholesky test device of the reference is out of scope
+        Discretization(spec, solver="direct")
+
+
+def test_initial_vector_is_nodal_interpolation():
+    spec, c = make()
+    x, y = spec.grid.interior_nodes()
+    assert initial_vector(spec) == pytest.approx(c["exact"](x, y, 0.0))
+
+
+@pytest.mark.parametrize("pre", PRECONDS)
+def test_implicit_solve_and_propagate_match_dense_solves(pre):
+    spec, _ = make(M=8)
+    disc = Discretization(spec, cg_opts=CgOptions(rel_tol=1e-13, preconditioner=pre))
+    ops = dense_ops(spec)
+    rng = np.random.default_rng(0)
+    dt = 0.125
+    imp, exp = ops.step_dense(dt, +1), ops.step_dense(dt, -1)
+    assert np.allclose(disc.combined(dt, +1).dense(), imp, rtol=1e-13, atol=0)
+    rhs = rng.standard_normal(disc.ndof)
+    assert host(disc.implicit_solve(dt, rhs)) == pytest.approx(np.linalg.solve(imp, rhs), abs=1e-10)
+    v = rng.standard_normal(disc.ndof)
+    assert host(disc.propagate(dt, v)) == pytest.approx(np.linalg.solve(imp, exp @ v), abs=1e-10)
+
+
+def test_solve_counters():
+    spec, _ = make()
+    disc = Discretization(spec)
+    assert disc.spatial_solves == 0
+    disc.implicit_solve(0.1, np.ones(disc.ndof))
+    assert disc.spatial_solves == 1
+    assert disc.cg_iterations > 0
+
+
+def test_load_vectors():
+    spec, _ = make()
+    silent = ProblemSpec(spec.grid, spec.tmesh, spec.kx, spec.ky, spec.beta, spec.gamma,
+                         source=lambda x, y, t: np.zeros_like(x), initial=spec.initial)
+    disc = Discretization(silent)
+    assert disc.load_vector(0.0, 0.25) == pytest.approx(np.zeros(disc.ndof))
+    with pytest.raises(ValueError):
+        load_vector(spec, 0)
+    with pytest.raises(ValueError):
+        load_vector(spec, 99)
+
+
+# ---- step / sequential_solve / spacetime_residual (test_stepper.py:98-140) ---------------------------------------
+@pytest.mark.parametrize("pre", PRECONDS)
+def test_step_matches_dense_solve(pre):
+    spec, _ = make(M=8)
+    disc = Discretization(spec, cg_opts=CgOptions(rel_tol=1e-13, preconditioner=pre))
+    ops = dense_ops(spec)
+    u0 = initial_vector(spec)
+    dt = spec.tmesh.widths[0]
+    expected = np.linalg.solve(ops.step_dense(dt, +1), disc.load_vector(0.0, dt) + ops.step_dense(dt, -1) @ u0)
+    assert host(step(spec, 1, u0, disc)) == pytest.approx(expected, abs=1e-11)
+
+
+@pytest.mark.parametrize("pre", PRECONDS)
+def test_sequential_solution_and_its_residual(pre):
+    spec, _ = make(M=8, N=8)
+    disc = Discretization(spec, cg_opts=CgOptions(rel_tol=1e-13, preconditioner=pre))
+    U = host(sequential_solve(spec, disc)).copy()
+    assert U.shape == (9, spec.grid.ndof)
+    assert U[0] == pytest.approx(initial_vector(spec))
+    _, res = spacetime_residual(spec, U, disc)
+    assert res < 1e-10
+    U[3] += 1e-3
+    norms, res = spacetime_residual(spec, U, disc)
+    assert res > 1e-5
+    assert norms[3] > 1e-5 and norms[4] > 1e-6 and norms[6] < 1e-10  # the perturbed point and its successor only
+    with pytest.raises(ValueError):
+        spacetime_residual(spec, U[:-1], disc)
+
+
+def test_solution_tracks_exact_solution():
+    errs = []
+    for M in (4, 8):
+        spec, c = make(M=M, N=M)
+        U = host(sequential_solve(spec))
+        x, y = spec.grid.interior_nodes()
+        errs.append(np.abs(U[-1] - c["exact"](x, y, 1.0)).max())
+    assert errs[1] < errs[0]
+
+
+# ---- solve (test_mgrit.py:139-200) ---------------------------------------------------------------------------------
+@pytest.mark.parametrize("pre", PRECONDS)
+def test_converges_and_matches_sequential(pre):
+    spec, _ = make(N=16)
+    U, trace = solve(spec, MgritOptions(m=4, halt_tol=1e-10, cg_rel_tol=1e-13, cg_preconditioner=pre))
+    assert trace.converged
+    disc = Discretization(spec, cg_opts=CgOptions(rel_tol=1e-13, preconditioner=pre))
+    _, res = spacetime_residual(spec, U, disc)
+    assert res < 1e-8
+    assert np.abs(U - host(sequential_solve(spec, disc))).max() < 1e-8
+
+
+def test_trace_contents_and_seeds():
+    spec, _ = make(N=16)
+    _, trace = solve(spec, MgritOptions(m=4, cg_rel_tol=1e-12))
+    assert trace.iterations == len(trace.residual_norms) - 1
+    assert len(trace.spatial_solves) == len(trace.residual_norms)
+    assert trace.spatial_solves == sorted(trace.spatial_solves)
+    assert all(t2 >= t1 for t1, t2 in zip(trace.wall_times, trace.wall_times[1:]))
+    assert trace.seed == 0
+    opts = MgritOptions(m=2, cg_rel_tol=1e-12, rng_seed=5)
+    _, t1 = solve(spec, opts)
+    _, t2 = solve(spec, opts)
+    assert t1.residual_norms == t2.residual_norms  # bitwise: deterministic reductions, same seed
+    _, t3 = solve(spec, MgritOptions(m=2, cg_rel_tol=1e-12, rng_seed=1))
+    assert t3.residual_norms[0] != t1.residual_norms[0]
+
+
+@pytest.mark.parametrize("pre", PRECONDS)
+def test_multilevel_matches_two_level_and_parareal_matches_sequential(pre):
+    spec, _ = make(N=64)
+    cg = CgOptions(rel_tol=1e-13, preconditioner=pre)
+    expected = host(sequential_solve(spec, Discretization(spec, cg_opts=cg)))
+    for levels in (2, None):
+        U, _ = solve(spec, MgritOptions(m=4, max_levels=levels, halt_tol=1e-11, cg_rel_tol=1e-13,
+                                        cg_preconditioner=pre))
+        assert np.abs(U - expected).max() < 1e-8
+    spec16, _ = make(N=16)
+    U, trace = parareal_solve(spec16, MgritOptions(m=4, halt_tol=1e-10, cg_rel_tol=1e-13, cg_preconditioner=pre))
+    assert trace.converged
+    assert np.abs(U - host(sequential_solve(spec16, Discretization(spec16, cg_opts=cg)))).max() < 1e-8
