@@ -170,3 +170,104 @@ def test_coarse_correction_touches_c_points_only(pre):
             assert np.array_equal(U[n], before[n] + Uc[n // 4])
         else:
             assert np.array_equal(U[n], before[n])
+
+
+# ---- one full two-level cycle against dense algebra (reference tests/test_acceptance.py:293-323, criterion 7) ------
+def dense_two_level_propagator(prob: O.Problem, m: int) -> np.ndarray:
+    """C-point error propagator of one FCF two-level cycle with re-discretised coarse steps, from dense step matrices:
+    J = (I - B^-1 A)(I - A), (A e)_k = e_k - Psi_k e_{k-1} (Psi_k = product of the interval's fine propagators),
+    (B e)_k = e_k - Phi_c,k e_{k-1} (one coarse step); k = 0 is the fixed initial value.  Built here from the oracle's
+    dense operators -- the reference's error_propagation_oracle (theory.py) is host analysis outside the hot path."""
+    ops = O.Operators(prob.grid, prob.kx, prob.ky, prob.beta, prob.gamma)
+    n = prob.grid.ndof
+    pts = prob.points
+    N = pts.size - 1
+    Nc = N // m
+    phi = lambda dt: np.linalg.solve(ops.step_dense(dt, +1), ops.step_dense(dt, -1))  # noqa: E731
+    A = np.eye((Nc + 1) * n)
+    B = np.eye((Nc + 1) * n)
+    for k in range(1, Nc + 1):
+        psi = np.eye(n)
+        for j in range((k - 1) * m + 1, k * m + 1):
+            psi = phi(pts[j] - pts[j - 1]) @ psi
+        A[k * n:(k + 1) * n, (k - 1) * n:k * n] = -psi
+        B[k * n:(k + 1) * n, (k - 1) * n:k * n] = -phi(pts[k * m] - pts[(k - 1) * m])
+    I = np.eye((Nc + 1) * n)
+    return (I - np.linalg.solve(B, A)) @ (I - A)
+
+
+@pytest.mark.parametrize("pre", PRECONDS)
+@pytest.mark.parametrize("mesh_kind", ["uniform", "shishkin"])
+@pytest.mark.parametrize("m,N", [(2, 8), (4, 8), (2, 16), (4, 16)])
+def test_two_level_cycle_matches_dense_error_propagator(pre, mesh_kind, m, N):
+    from paper_1805_06688_b200.mesh import shishkin_temporal
+
+    c = manufactured(0.8, 0.7, 2.0, 0.5)
+    tm = uniform_temporal(1.0, N) if mesh_kind == "uniform" else shishkin_temporal(N, 2.0**-4)
+    spec = ProblemSpec(SpatialGrid(4, 4), tm, c["kx"], c["ky"], c["beta"], c["gamma"], c["source"], c["initial"])
+    prob = O.Problem(O.Grid(4, 4), tm.points, c["kx"], c["ky"], c["beta"], c["gamma"], c["source"], c["initial"])
+    hier = MgritHierarchy(spec, MgritOptions(m=m, max_levels=2, cg_rel_tol=TOL, cg_preconditioner=pre))
+    fine, coarse = hier.levels
+    exact = sequential_solve(spec, fine.disc)
+    exact = exact.cpu().numpy() if hasattr(exact, "cpu") else exact
+    err = np.random.default_rng(99).standard_normal(exact.shape)
+    err[0] = 0.0
+    fine.U.copy_(torch.from_numpy(exact + err))
+    fcf_relax(fine)
+    restrict_residual(hier, 0)
+    coarse.U.zero_()
+    exact_solve(coarse)
+    coarse_correct(hier, 0)
+    hier.check_fail()
+    got = (fine.U.cpu().numpy() - exact)[::m].ravel()
+    predicted = dense_two_level_propagator(prob, m) @ err[::m].ravel()
+    assert np.abs(got - predicted).max() <= 1e-9
+
+
+# ---- property suite across the parameter grid (test_acceptance.py:357-400, criterion 8) ----------------------------
+@pytest.mark.parametrize("m", [2, 4, 8, 16])
+@pytest.mark.parametrize("pair", [(0.6, 0.7), (0.8, 0.8), (0.95, 0.65)])
+def test_fcf_invariance_and_f_residuals_across_parameters(pair, m):
+    c = manufactured(*pair, 2.0, 0.5)
+    N = 4 * m
+    tm = uniform_temporal(1.0, N)
+    spec = ProblemSpec(SpatialGrid(4, 4), tm, c["kx"], c["ky"], c["beta"], c["gamma"], c["source"], c["initial"])
+    prob = O.Problem(O.Grid(4, 4), tm.points, c["kx"], c["ky"], c["beta"], c["gamma"], c["source"], c["initial"])
+    hier = MgritHierarchy(spec, MgritOptions(m=m, max_levels=2, cg_rel_tol=TOL))
+    fine = hier.levels[0]
+    st = O.Stepper(prob, rel_tol=TOL)
+    exact = O.sequential(prob, st)
+    fine.U.copy_(torch.from_numpy(exact))
+    fcf_relax(fine)
+    hier.check_fail()
+    assert np.abs(fine.U.cpu().numpy() - exact).max() < 1e-9
+    G = device_G(fine)
+    U0 = np.random.default_rng(0).random((N + 1, prob.grid.ndof))
+    U0[0] = G[0]
+    fine.U.copy_(torch.from_numpy(U0))
+    fine.ax_valid = False  # U was replaced behind the hierarchy's back
+    fcf_relax(fine)
+    hier.check_fail()
+    U = fine.U.cpu().numpy()
+    for n in range(1, N + 1):
+        if n % m:
+            r = G[n] + st.propagate(tm.points[n] - tm.points[n - 1], U[n - 1]) - U[n]
+            assert np.abs(r).max() < 1e-10
+
+
+@pytest.mark.parametrize("m", [2, 4, 8, 16])
+@pytest.mark.parametrize("pair", [(0.6, 0.7), (0.8, 0.8), (0.95, 0.65)])
+def test_per_iteration_ratio_respects_two_level_bound(pair, m):
+    from paper_1805_06688_b200.mgrit import solve
+    from paper_1805_06688_b200.theory import mode_spectrum, two_level_bound
+
+    c = manufactured(*pair, 2.0, 0.5)
+    spec = ProblemSpec(SpatialGrid(6, 6), uniform_temporal(1.0, 8 * m), c["kx"], c["ky"], c["beta"], c["gamma"],
+                       c["source"], c["initial"])
+    bound = two_level_bound(mode_spectrum(spec), spec.tmesh, m).bound
+    _, trace = solve(spec, MgritOptions(m=m, max_levels=2, halt_tol=1e-11, cg_rel_tol=TOL))
+    norms = trace.residual_norms
+    for r_prev, r_next in zip(norms[1:-1], norms[2:]):
+        if r_prev < 1e-11:  # measurement floor of the inner solves
+            continue
+        assert r_next / r_prev <= max(bound, 1e-10) * 1.05 + 1e-12
