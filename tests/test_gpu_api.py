@@ -20,8 +20,8 @@ pytestmark = pytest.mark.gpu
 PRECONDS = ["tau", "none"]
 
 
-def make(M=4, N=4, **over):
-    c = dict(manufactured(), **over)
+def make(M=4, N=4, **physics):
+    c = manufactured(**physics)  # the source term belongs to the orders and diffusivities
     return ProblemSpec(SpatialGrid(M, M), uniform_temporal(1.0, N), c["kx"], c["ky"], c["beta"], c["gamma"],
                        c["source"], c["initial"]), c
 
@@ -172,3 +172,56 @@ def test_multilevel_matches_two_level_and_parareal_matches_sequential(pre):
     U, trace = parareal_solve(spec16, MgritOptions(m=4, halt_tol=1e-10, cg_rel_tol=1e-13, cg_preconditioner=pre))
     assert trace.converged
     assert np.abs(U - host(sequential_solve(spec16, Discretization(spec16, cg_opts=cg)))).max() < 1e-8
+
+
+# ---- acceptance-style properties (reference tests/test_acceptance.py criteria 1-6, as properties: the published table
+# values themselves are not restated here) ---------------------------------------------------------------------------
+@pytest.mark.parametrize("pair", [(0.6, 0.7), (0.95, 0.65), (0.8, 0.8)])
+def test_second_order_convergence_under_refinement(pair):
+    """Simultaneous refinement M = N = 4 ... 32 (tau = h): the nodal error against the manufactured solution falls at
+    the scheme's second order once the grids resolve the solution (the reference asserts rates in [1.7, 2.3] on the
+    L2 error of the interpolant, which includes the O(h^2) interpolation error; the nodal maximum used here is
+    pre-asymptotic on the 4 -> 8 step)."""
+    errs = []
+    for M in (4, 8, 16, 32):
+        spec, c = make(M=M, N=M, beta=pair[0], gamma=pair[1])
+        U = host(sequential_solve(spec, Discretization(spec, cg_opts=CgOptions(rel_tol=1e-12))))
+        x, y = spec.grid.interior_nodes()
+        errs.append(max(np.abs(U[n] - c["exact"](x, y, spec.tmesh.points[n])).max() for n in range(M + 1)))
+    rates = [np.log2(a / b) for a, b in zip(errs, errs[1:])]
+    assert all(b < a for a, b in zip(errs, errs[1:])), errs
+    assert all(1.5 <= r <= 2.5 for r in rates[1:]), (errs, rates)
+
+
+@pytest.mark.parametrize("m", [2, 4, 8])
+def test_multilevel_mgrit_agrees_with_sequential_at_256_steps(m):
+    spec, _ = make(M=16, N=256, beta=0.6, gamma=0.7)
+    disc = Discretization(spec, cg_opts=CgOptions(rel_tol=1e-12))
+    U, trace = solve(spec, MgritOptions(m=m, halt_tol=1e-9, cg_rel_tol=1e-12))
+    assert trace.converged
+    _, res = spacetime_residual(spec, U, disc)
+    assert res <= 1e-8
+    if m == 8:
+        U, trace = parareal_solve(spec, MgritOptions(m=8, halt_tol=1e-9, cg_rel_tol=1e-12))
+        assert trace.converged
+        _, res = spacetime_residual(spec, U, disc)
+        assert res <= 1e-8
+
+
+@pytest.mark.parametrize("kind,m", [("uniform", 2), ("uniform", 16), ("shishkin", 4), ("shishkin", 8)])
+def test_observed_two_level_factor_never_exceeds_the_bound(kind, m):
+    from paper_1805_06688_b200.mesh import shishkin_temporal
+    from paper_1805_06688_b200.mgrit import MgritFailure, convergence_factor
+    from paper_1805_06688_b200.theory import mode_spectrum, two_level_bound
+
+    c = manufactured(0.95, 0.65, 2.0, 0.5) if kind == "uniform" else manufactured(0.95, 0.65, 3.0, 7.5)
+    tm = uniform_temporal(1.0, 512) if kind == "uniform" else shishkin_temporal(512, 2.0**-6)
+    spec = ProblemSpec(SpatialGrid(8, 8), tm, c["kx"], c["ky"], c["beta"], c["gamma"], c["source"], c["initial"])
+    bound = two_level_bound(mode_spectrum(spec), spec.tmesh, m).bound
+    try:
+        _, trace = solve(spec, MgritOptions(m=m, max_levels=2, halt_tol=1e-12, max_iters=300, cg_rel_tol=1e-14))
+    except MgritFailure as exc:
+        trace = exc.trace
+    observed = convergence_factor(trace)
+    assert 0.0 < bound < 1.0
+    assert observed <= bound * 1.02
