@@ -42,6 +42,9 @@
 #ifndef RM_CNT_T
 #define RM_CNT_T int64_t  // per-solve iteration / apply counters
 #endif
+#ifndef RM_POLL_RELAXED
+#define RM_POLL_RELAXED 0  // group barrier: relaxed polls + one acquire fence (1) or acquire polls (0)
+#endif
 #ifndef RM_STORE_NB
 #define RM_STORE_NB 4  // column-store batch
 #endif
@@ -301,11 +304,21 @@ __device__ __forceinline__ void gsync(Sync& sy) {
     // release-add: the CTA's writes (ordered before by the CTA barrier) become visible with the arrival
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(sy.gbar) : "memory");
     const unsigned target = sy.epoch * (unsigned)G;
+#if RM_POLL_RELAXED
+    // relaxed polls, one acquire fence after the last: an acquire load costs an L1 invalidation (CCTL.IVALL) per poll
+    for (;;) {
+      unsigned v;
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(sy.gbar) : "memory");
+      if (v >= target) break;
+    }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#else
     for (;;) {
       unsigned v;
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(sy.gbar) : "memory");
       if (v >= target) break;
     }
+#endif
   }
   __syncthreads();
 }
